@@ -1,0 +1,448 @@
+#!/usr/bin/env python
+"""BBWADG hot-path benchmark: DOF-stage updates/s per B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--config 5|3|4] [--N n --M m] [--dtype f64|f32] [--sweep]
+
+A "step" is one LSRK45 step = 5 fused RK stages (volume + surface + WADG
+multiply/project + LSRK update) over every element of the workload.
+
+Default workload (``config.workload``): BASELINE config 5 per GPU -- a Kuhn-cube
+mesh of 88^3 cubes = 4,088,832 tets per GPU (weak scaling: boxes 176x88x88,
+176x176x88, 176^3 at 2/4/8 GPUs, element-partitioned with the NCCL face-trace
+halo), N=7, M=4, smooth c^2 = 1 + 1/2 sin(pi x) sin(pi y) sin(pi z) projected to
+P^4, fp64.  Inputs are synthetic (seeded) and far larger than L2 (state 15.7 GB
+per GPU), so no L2 flush is needed between timed steps.
+
+value      = 4 * K_total * Np * 5 * K_steps / (max over ranks of the device time of
+             the K timed steps), CUDA events on the library's stream;
+e2e        = the same metric through the public API with host buffers:
+             bbwadg_set_state(pinned host) + K x bbwadg_run(1 step; includes the
+             device->host read of the finiteness flag) + bbwadg_get_state(pinned host);
+roofline   = the stage kernel: algorithmic bytes per launch / average launch time
+             vs the measured HBM copy peak (MEASURED_PEAKS.json);
+cpu_baseline = the CPU oracle (oracle/, test infrastructure) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from math import comb
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DOF-stage updates/sec per B200 (BBWADG acoustic RK stage, fused RHS + LSRK45)"
+UNIT = "DOF-stage/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def factor_cuts(p: int):
+    best = None
+    for px in range(1, p + 1):
+        for py in range(1, px + 1):
+            if p % (px * py):
+                continue
+            pz = p // (px * py)
+            if pz > py:
+                continue
+            sc = px - pz
+            if best is None or sc < best[0]:
+                best = (sc, (px, py, pz))
+    return best[1]
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return pk, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_workload(args, rank, world, device=None):
+    from workloads import kuhn, media
+
+    n = args.n_cubes
+    if args.config == 5:
+        cuts = factor_cuts(world)
+        shape = (n * cuts[0], n * cuts[1], n * cuts[2])
+        h = 2.0 / n
+        v, e = kuhn.kuhn_mesh(shape, h=h)
+        cfunc = media.c2_smooth(1.0)
+        name = f"config5: Kuhn {shape[0]}x{shape[1]}x{shape[2]} cubes ({n}^3 = {6 * n ** 3:,} tets per GPU), smooth c^2 k=1"
+    elif args.config == 3:
+        cuts = factor_cuts(world)
+        v, e = kuhn.kuhn_mesh((n * cuts[0], n * cuts[1], n * cuts[2]), h=2.0 / n)
+        cfunc = media.c2_smooth(8.0)
+        name = f"config3: Kuhn {n}^3 cubes per GPU ({6 * n ** 3:,} tets), sub-cell c^2 k=8"
+    elif args.config == 4:
+        cuts = factor_cuts(world)
+        v, e = kuhn.kuhn_mesh((n * cuts[0], n * cuts[1], n * cuts[2]), h=2.0 / n)
+        cfunc = media.c2_layered()
+        name = f"config4: Kuhn {n}^3 cubes per GPU ({6 * n ** 3:,} tets), layered c^2"
+    else:
+        raise SystemExit("unknown config")
+    return v, e, cfunc, cuts, name
+
+
+def local_c2(v, e, cfunc, M, rank, world, cuts, device):
+    """c^2_M for the elements this rank owns (rows of other ranks are ignored by the library:
+    filled with 1.0)."""
+    from paper_1808_08645_b200 import lib as L
+    from workloads import media
+
+    Mp = comb(M + 3, 3)
+    if world == 1:
+        return media.project_c2(v, e, cfunc, M, device=device), None
+    plan = L.bbwadg_partition_plan(v, e, world, rank, cuts)
+    gid = plan["gid"]
+    c2 = np.ones((e.shape[0], Mp))
+    c2[gid] = media.project_c2(v, e[gid], cfunc, M, device=device)
+    return c2, gid
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1808_08645_b200 import Solver
+    from paper_1808_08645_b200 import lib as L
+
+    N, M = args.N, args.M
+    Np = comb(N + 3, 3)
+    v, e, cfunc, cuts, wname = build_workload(args, rank, world, device=dev)
+    c2, _ = local_c2(v, e, cfunc, M, rank, world, cuts, dev)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+
+        idbuf = [L.bbwadg_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idbuf, src=0)
+        nccl_id = idbuf[0]
+    stream = torch.cuda.current_stream(dev)
+    s = Solver(v, e, N, M, c2, dtype=args.dtype, device=local, stream=stream, rank=rank, world_size=world,
+               nccl_id=nccl_id, partition=cuts if world > 1 else None)
+    info = s.info()
+    K_local = info["num_elements_local"]
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1808 + rank)
+    Q0 = torch.randn((K_local, 4, Np), dtype=tdt, device=dev, generator=gen)
+    s.set_state(Q0)
+    del Q0
+    h_min = 2.0 / args.n_cubes / (1 + np.sqrt(2) + np.sqrt(3))  # Kuhn tet inradius-scale height bound
+    dt = 0.5 * h_min / (np.sqrt(1.5) * (N + 1) ** 2)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for i in range(args.warmup):
+        s.step(i * dt, dt)
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            s.step((args.warmup + i) * dt, dt)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = ms
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    K_total = info["num_elements_global"]
+    dof_stage = 4.0 * K_total * Np * 5 * args.steps
+    value = dof_stage / (ms_max / 1e3)
+    launches = info["kernels_per_stage"] * 5 * args.steps
+
+    # roofline of the stage kernel (only kernel at N=1: ms / launches is its average duration)
+    peaks, peak_kind = load_peaks()
+    stage_launches = 5 * args.steps * (2 if world > 1 else 1)
+    avg_launch_s = ms / 1e3 / (5 * args.steps) if world == 1 else ms / 1e3 / (5 * args.steps)
+    bytes_per_stage = info["algorithmic_bytes_per_stage"]
+    achieved = bytes_per_stage / avg_launch_s / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as fh:
+                tr = json.load(fh).get(f"N{N}M{M}{args.dtype}")
+            if tr:
+                traffic = tr["dram_bytes_per_launch"] * (K_local / tr["K_local"])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs (copy)" if peak_kind == "measured" else "fallback",
+                "kernel": f"bbw::stage_kernel<N={N},M={M},{args.dtype}>",
+                "algorithmic_bytes_per_launch": bytes_per_stage,
+                "flops_per_launch": info["flops_per_stage"],
+                "achieved_tflops": round(info["flops_per_stage"] / avg_launch_s / 1e12, 3)}
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hostQ = torch.empty((K_local, 4, Np), dtype=tdt, pin_memory=True)
+        hostQ.normal_(generator=torch.Generator().manual_seed(1808 + rank)) if args.e2e_random else hostQ.fill_(0.5)
+        hQ = hostQ.numpy()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        L.bbwadg_set_state(s.ctx, hQ, 0)
+        for i in range(args.steps):
+            L.bbwadg_run(s.ctx, i * dt, dt, 1)
+        L.bbwadg_get_state(s.ctx, hQ, 0)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        el = t1 - t0
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        sb = K_local * 4 * Np * (8 if args.dtype == "f64" else 4)
+        e2e = {"value": dof_stage / el, "unit": UNIT, "h2d_bytes_per_step": sb / args.steps,
+               "d2h_bytes_per_step": (sb + 4 * args.steps) / args.steps,
+               "how": "bbwadg_set_state(pinned host) + K x bbwadg_run(1 step, D2H finiteness flag) + "
+                      "bbwadg_get_state(pinned host), host wall clock, max over ranks"}
+        del hostQ
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+           "config": {"workload": wname, "N": N, "M": M, "K_total": K_total, "K_per_gpu": K_local,
+                      "Np": Np, "dofs_per_stage": 4 * K_total * Np,
+                      "parallelism": f"element-partitioned x{world} (RCB cuts {list(cuts)}) + NCCL face-trace halo"
+                      if world > 1 else "single GPU",
+                      "l2": "inputs (state %.1f GB/GPU) far larger than the 126 MB L2; no flush needed"
+                            % (K_local * 4 * Np * (8 if args.dtype == 'f64' else 4) / 1e9)},
+           "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
+    s.close()
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(N, M, args.cpu_seconds)
+    if rank == 0 and args.sweep:
+        out["sweep"] = sweep(args, dev)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def sweep(args, dev):
+    """BASELINE config 3: N = 1..9, M = N on the n=44 Kuhn mesh (511,104 tets), fp64."""
+    import torch
+
+    from paper_1808_08645_b200 import Solver
+    from workloads import kuhn, media
+
+    v, e = kuhn.kuhn_mesh(args.sweep_n)
+    f = media.c2_smooth(8.0)
+    peaks, _ = load_peaks()
+    rows = []
+    for N in range(1, 10):
+        M = N
+        Np = comb(N + 3, 3)
+        c2 = media.project_c2(v, e, f, M, device=dev)
+        s = Solver(v, e, N, M, c2, device=dev.index, stream=torch.cuda.current_stream(dev), check_c2=False)
+        Q0 = torch.randn((len(e), 4, Np), dtype=torch.float64, device=dev)
+        s.set_state(Q0)
+        del Q0
+        for i in range(2):
+            s.step(0.0, 1e-4)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nst = 5
+        a.record()
+        for i in range(nst):
+            s.step(0.0, 1e-4)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / nst
+        info = s.info()
+        gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
+        rows.append({"N": N, "M": M, "value": 4.0 * len(e) * Np * 5 / (ms / 1e3), "ms_per_step": ms,
+                     "ns_per_element_stage": ms * 1e6 / (5 * len(e)), "hbm_frac": gbs / peaks["hbm_gbs"],
+                     "tflops": info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12})
+        s.close()
+    Ns = np.array([r["N"] for r in rows if r["N"] >= 4], dtype=float)
+    ts = np.array([r["ns_per_element_stage"] for r in rows if r["N"] >= 4])
+    slope = float(np.polyfit(np.log(Ns), np.log(ts), 1)[0])
+    return {"workload": f"config3: Kuhn n={args.sweep_n} ({len(e):,} tets), M=N, c^2 k=8, fp64",
+            "rows": rows, "loglog_slope_time_per_element_N4to9": slope}
+
+
+def cpu_baseline(N, M, seconds):
+    """The CPU oracle as it stands, timed on this host on a bounded sample."""
+    import threadpoolctl
+
+    from oracle.acoustic import AcousticOracle
+    from workloads import kuhn, media, states
+
+    n = 4 if N >= 7 else 6
+    v, e = kuhn.kuhn_mesh(n)
+    c2 = media.project_c2(v, e, media.c2_smooth(1.0), M)
+    Q = states.random_state(len(e), N)
+    t0 = time.perf_counter()
+    o = AcousticOracle(v, e, N, M, c2)
+    setup = time.perf_counter() - t0
+    res = np.zeros_like(Q)
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        o.step(Q, res, 0.0, 1e-4)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el > seconds or steps >= 50:
+            break
+    Np = comb(N + 3, 3)
+    info = threadpoolctl.threadpool_info()
+    cores = max([i.get("num_threads", 1) for i in info] + [1])
+    return {"value": 4.0 * len(e) * Np * 5 * steps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{steps} LSRK45 step(s) of the oracle on a {len(e)}-tet Kuhn mesh (n={n}), N={N}, M={M}, "
+                      f"fp64 numpy/BLAS; table setup {setup:.1f}s excluded",
+            "cpu": os.uname().machine, "os_cpu_count": os.cpu_count()}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cb = cpu_baseline(args.N, args.M, args.cpu_seconds)
+    wname = f"config{args.config} (oracle on a bounded sample: {cb['sample']})"
+    per_step_ms = 4.0 * 6 * args.n_cubes ** 3 * comb(args.N + 3, 3) * 5 / cb["value"] * 1e3
+    out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+           "config": {"workload": wname, "N": args.N, "M": args.M},
+           "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                       "d2h_bytes_per_step": 0}, "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--N", type=int, default=None)
+    ap.add_argument("--M", type=int, default=None)
+    ap.add_argument("--n-cubes", type=int, default=None)
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
+    ap.add_argument("--sweep", action="store_true", help="append the config-3 N=1..9 sweep")
+    ap.add_argument("--sweep-n", type=int, default=44)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-random", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    defaults = {5: (7, 4, 88), 3: (7, 7, 44), 4: (5, 3, 56)}
+    dN, dM, dn = defaults.get(args.config, (7, 4, 88))
+    args.N = args.N if args.N is not None else dN
+    args.M = args.M if args.M is not None else dM
+    args.n_cubes = args.n_cubes if args.n_cubes is not None else dn
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

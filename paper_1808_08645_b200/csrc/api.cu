@@ -1,0 +1,764 @@
+// extern "C" implementation of include/bbwadg.h.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/bbwadg.h"
+#include "dispatch.hpp"
+#include "mesh.hpp"
+#include "nccl_shim.hpp"
+#include "stage_kernel.cuh"
+#include "tables.hpp"
+
+using namespace bbw;
+
+namespace bbw {
+KernelSet get_kernels(int N, int M, int dtype) {
+  switch (N) {
+    case 1: return get_kernels_N1(M, dtype);
+    case 2: return get_kernels_N2(M, dtype);
+    case 3: return get_kernels_N3(M, dtype);
+    case 4: return get_kernels_N4(M, dtype);
+    case 5: return get_kernels_N5(M, dtype);
+    case 6: return get_kernels_N6(M, dtype);
+    case 7: return get_kernels_N7(M, dtype);
+    case 8: return get_kernels_N8(M, dtype);
+    case 9: return get_kernels_N9(M, dtype);
+    default: return KernelSet();
+  }
+}
+}  // namespace bbw
+
+// Carpenter & Kennedy (1994) 5-stage 2N-storage RK4 (R13)
+static const double RK_A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                               -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+static const double RK_B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                               1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                               2277821191437.0 / 14882151754819.0};
+static const double RK_C[5] = {0.0, 1432997174477.0 / 9575080441755.0, 2526269341429.0 / 6820363962896.0,
+                               2006345519317.0 / 3224310063776.0, 2802321613138.0 / 2924317926251.0};
+
+static thread_local std::string g_last_error;
+
+struct Group;
+
+struct bbwadg_ctx_s {
+  int N = 0, M = 0, dtype = 0, device = 0, Np = 0, Mp = 0, Nfp = 0;
+  size_t rb = 8;  // bytes per real
+  double tau_p = 1, tau_u = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t K_global = 0;
+  Part part;
+  HostTables tables;
+  KernelSet ks;
+  int grid = 0;
+  // device memory
+  void* d_tab = nullptr;
+  void* d_Q[2] = {nullptr, nullptr};
+  int cur = 0;
+  void* d_res = nullptr;
+  void* d_c2 = nullptr;
+  void* d_geo = nullptr;
+  int* d_nbr = nullptr;
+  uint8_t* d_code = nullptr;
+  void* d_src = nullptr;
+  void* d_ghost = nullptr;
+  void* d_send = nullptr;
+  int* d_sendfaces = nullptr;
+  int* d_flag = nullptr;
+  // multi-GPU
+  nccl::Comm comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  Group* group = nullptr;
+  int group_index = 0;
+  // bookkeeping
+  int64_t steps = 0;
+  double t = 0;
+  std::string err;
+};
+
+struct Group {
+  std::vector<bbwadg_ctx> parts;
+  cudaStream_t stream = nullptr;  // shared by all members, owned by the group
+};
+
+namespace {
+
+bbwadg_status fail(bbwadg_ctx c, bbwadg_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  g_last_error = msg;
+  return s;
+}
+
+#define CUDA_TRY(ctx, call)                                                                          \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? BBWADG_ERR_OOM : BBWADG_ERR_CUDA,           \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                               \
+    }                                                                                                \
+  } while (0)
+
+template <typename R>
+void fill_args(bbwadg_ctx c, StageArgs<R>& a) {
+  std::memset(&a, 0, sizeof(a));
+  a.c2 = static_cast<const R*>(c->d_c2);
+  a.geo = static_cast<const R*>(c->d_geo);
+  a.nbr = c->d_nbr;
+  a.code = c->d_code;
+  a.ghost = static_cast<const R*>(c->d_ghost);
+  a.src = static_cast<const R*>(c->d_src);
+  a.tab = static_cast<const uint8_t*>(c->d_tab);
+  const HostTables& T = c->tables;
+  a.off = TableOffsets{(uint32_t)T.off_up,     (uint32_t)T.off_dn,      (uint32_t)T.off_dec,
+                       (uint32_t)T.off_fnode,  (uint32_t)T.off_nbrvol,  (uint32_t)T.off_nbrface,
+                       (uint32_t)T.off_triup,  (uint32_t)T.off_l0,      (uint32_t)T.off_lgather,
+                       (uint32_t)T.off_invfactN, (uint32_t)T.off_invfactM, (uint32_t)T.off_post};
+  a.tau_p = (R)c->tau_p;
+  a.tau_u = (R)c->tau_u;
+  for (int j = 0; j < 10; ++j) {
+    a.cj[j] = (R)T.cj[j];
+    a.lj[j] = (R)T.lj[j];
+  }
+}
+
+// Launch one kernel pass over local elements [b, e).
+bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e, double rk_a,
+                          double rk_b, double dt, double tstage) {
+  if (e <= b) return BBWADG_OK;
+  int64_t nb = (e - b + c->ks.elems_per_cta - 1) / c->ks.elems_per_cta;
+  int grid = (int)std::min<int64_t>(nb, c->grid);
+  cudaError_t err;
+  if (c->dtype == BBWADG_F64) {
+    StageArgs<double> a;
+    fill_args(c, a);
+    a.Qin = static_cast<const double*>(Qin);
+    a.Qout = static_cast<double*>(Qout);
+    a.res = static_cast<double*>(c->d_res);
+    a.elem_begin = b;
+    a.elem_end = e;
+    a.rk_a = rk_a;
+    a.rk_b = rk_b;
+    a.dt = dt;
+    a.src_amp = std::sin(M_PI * tstage);
+    a.mode = mode;
+    err = c->ks.launch_stage(&a, grid, c->stream);
+  } else {
+    StageArgs<float> a;
+    fill_args(c, a);
+    a.Qin = static_cast<const float*>(Qin);
+    a.Qout = static_cast<float*>(Qout);
+    a.res = static_cast<float*>(c->d_res);
+    a.elem_begin = b;
+    a.elem_end = e;
+    a.rk_a = (float)rk_a;
+    a.rk_b = (float)rk_b;
+    a.dt = (float)dt;
+    a.src_amp = (float)std::sin(M_PI * tstage);
+    a.mode = mode;
+    err = c->ks.launch_stage(&a, grid, c->stream);
+  }
+  if (err != cudaSuccess) return fail(c, BBWADG_ERR_CUDA, std::string("stage kernel launch: ") + cudaGetErrorString(err));
+  return BBWADG_OK;
+}
+
+const uint16_t* fnode_ptr(bbwadg_ctx c) {
+  return reinterpret_cast<const uint16_t*>(static_cast<const uint8_t*>(c->d_tab) + c->tables.off_fnode);
+}
+
+// NCCL halo for source state Q: pack on the comm stream, grouped send/recv, event.
+bbwadg_status halo_nccl(bbwadg_ctx c, const void* Q) {
+  const Part& P = c->part;
+  const int64_t nsend = P.send_off.back();
+  CUDA_TRY(c, cudaEventRecord(c->ev_ready, c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+  CUDA_TRY(c, c->ks.launch_pack(Q, c->d_sendfaces, (int)nsend, fnode_ptr(c), c->d_send, c->comm_stream));
+  const size_t per_face = 4 * (size_t)c->Nfp;
+  int dt = c->dtype == BBWADG_F64 ? nccl::kDouble : nccl::kFloat;
+  if (nccl::group_start() != 0) return fail(c, BBWADG_ERR_NCCL, "ncclGroupStart failed");
+  for (int r = 0; r < P.nparts; ++r) {
+    int64_t ns = P.send_off[r + 1] - P.send_off[r];
+    int64_t nr = P.recv_off[r + 1] - P.recv_off[r];
+    if (ns > 0) {
+      const char* sp = static_cast<const char*>(c->d_send) + P.send_off[r] * per_face * c->rb;
+      if (nccl::send(sp, ns * per_face, dt, r, c->comm, c->comm_stream) != 0)
+        return fail(c, BBWADG_ERR_NCCL, "ncclSend failed");
+    }
+    if (nr > 0) {
+      char* rp = static_cast<char*>(c->d_ghost) + P.recv_off[r] * per_face * c->rb;
+      if (nccl::recv(rp, nr * per_face, dt, r, c->comm, c->comm_stream) != 0)
+        return fail(c, BBWADG_ERR_NCCL, "ncclRecv failed");
+    }
+  }
+  if (nccl::group_end() != 0) return fail(c, BBWADG_ERR_NCCL, std::string("ncclGroupEnd failed: ") + nccl::last_error(c->comm));
+  CUDA_TRY(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+  return BBWADG_OK;
+}
+
+// One pass (stage or rhs) over all local elements including the halo exchange when partitioned.
+bbwadg_status full_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, double rk_a, double rk_b, double dt,
+                        double tstage) {
+  const Part& P = c->part;
+  if (P.nparts > 1 && c->comm) {
+    bbwadg_status s = halo_nccl(c, Qin);
+    if (s) return s;
+    s = launch_pass(c, mode, Qin, Qout, 0, P.n_interior, rk_a, rk_b, dt, tstage);
+    if (s) return s;
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    return launch_pass(c, mode, Qin, Qout, P.n_interior, P.K_local, rk_a, rk_b, dt, tstage);
+  }
+  return launch_pass(c, mode, Qin, Qout, 0, P.K_local, rk_a, rk_b, dt, tstage);
+}
+
+size_t state_bytes(bbwadg_ctx c) { return (size_t)c->part.K_local * 4 * c->Np * c->rb; }
+
+template <typename R>
+__global__ void nonfinite_kernel(const R* __restrict__ q, long long n, int* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(q[i])) {
+      *flag = 1;
+      return;
+    }
+}
+
+bbwadg_status upload_real(bbwadg_ctx c, void** dst, const std::vector<double>& host) {
+  size_t n = host.size();
+  if (n == 0) {
+    *dst = nullptr;
+    return BBWADG_OK;
+  }
+  CUDA_TRY(c, cudaMalloc(dst, n * c->rb));
+  if (c->dtype == BBWADG_F64) {
+    CUDA_TRY(c, cudaMemcpy(*dst, host.data(), n * 8, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> f(host.begin(), host.end());
+    CUDA_TRY(c, cudaMemcpy(*dst, f.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  return BBWADG_OK;
+}
+
+// c^2_M at the vertices and at interior sample points (R16): Bernstein evaluation by
+// de Casteljau-free direct formula in long double.
+bool c2_positive(const double* c2, int M, std::string& why, int64_t k) {
+  // sample: vertices + a barycentric lattice of degree M+2
+  int q = M + 2;
+  auto idx = indices3(M);
+  for (int b3 = 0; b3 <= q; ++b3)
+    for (int b2 = 0; b2 <= q - b3; ++b2)
+      for (int b1 = 0; b1 <= q - b3 - b2; ++b1) {
+        long double lam[4] = {(long double)(q - b1 - b2 - b3) / q, (long double)b1 / q, (long double)b2 / q,
+                              (long double)b3 / q};
+        long double v = 0;
+        for (size_t i = 0; i < idx.size(); ++i) {
+          long double term = 1;
+          int fac = 1;
+          for (int m = 2; m <= M; ++m) fac *= m;
+          long double mult = fac;
+          for (int j = 0; j < 4; ++j) {
+            for (int m = 2; m <= idx[i].a[j]; ++m) mult /= m;
+            for (int p = 0; p < idx[i].a[j]; ++p) term *= lam[j];
+          }
+          v += mult * term * c2[i];
+        }
+        if (!(v > 0)) {
+          std::ostringstream os;
+          os << "c^2_M is not positive in element " << k << " (value " << (double)v << ")";
+          why = os.str();
+          return false;
+        }
+      }
+  return true;
+}
+
+bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, const bbwadg_options& o, int rank,
+                        int nparts, cudaStream_t shared_stream, bbwadg_ctx* out) {
+  std::unique_ptr<bbwadg_ctx_s> c(new bbwadg_ctx_s());
+  c->N = N;
+  c->M = M;
+  c->dtype = o.dtype;
+  c->device = o.device;
+  c->rb = o.dtype == BBWADG_F64 ? 8 : 4;
+  c->tau_p = o.tau_p;
+  c->tau_u = o.tau_u;
+  c->Np = np3(N);
+  c->Mp = np3(M);
+  c->Nfp = np2(N);
+  c->K_global = g.K;
+  CUDA_TRY(c.get(), cudaSetDevice(o.device));
+  c->ks = get_kernels(N, M, o.dtype);
+  if (!c->ks.launch_stage) return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "no kernel instantiation for this (N, M, dtype)");
+  CUDA_TRY(c.get(), c->ks.prepare());
+  int nsm = 0;
+  CUDA_TRY(c.get(), cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
+  c->grid = nsm * c->ks.blocks_per_sm();
+  // NULL selects the legacy default stream (stream 0), so that work is ordered with
+  // torch's default stream and every other legacy-stream user (cuBLAS convention).
+  c->stream = shared_stream ? shared_stream : static_cast<cudaStream_t>(o.cuda_stream);
+  c->own_stream = false;
+  c->part = build_part(g, rank, nparts);
+  const Part& P = c->part;
+  // tables
+  try {
+    c->tables = build_tables(N, M, (int)c->rb);
+  } catch (const std::exception& e) {
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, e.what());
+  }
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_tab, c->tables.blob.size()));
+  CUDA_TRY(c.get(), cudaMemcpy(c->d_tab, c->tables.blob.data(), c->tables.blob.size(), cudaMemcpyHostToDevice));
+  // per-element inputs in local order
+  const int64_t KL = P.K_local;
+  std::vector<double> geo(12 * KL), c2l((size_t)KL * c->Mp);
+  for (int64_t i = 0; i < KL; ++i) {
+    element_gradients(g, P.gid[i], &geo[12 * i]);
+    std::memcpy(&c2l[(size_t)i * c->Mp], c2 + (size_t)P.gid[i] * c->Mp, sizeof(double) * c->Mp);
+    if (o.check_c2) {
+      std::string why;
+      if (!c2_positive(c2 + (size_t)P.gid[i] * c->Mp, M, why, P.gid[i])) {
+        bbwadg_ctx raw = c.release();
+        bbwadg_destroy(raw);
+        return fail(nullptr, BBWADG_ERR_NONPOSITIVE_C2, why);
+      }
+    }
+  }
+  bbwadg_status s;
+  if ((s = upload_real(c.get(), &c->d_geo, geo))) return fail(nullptr, s, c->err);
+  if ((s = upload_real(c.get(), &c->d_c2, c2l))) return fail(nullptr, s, c->err);
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_nbr, sizeof(int) * 4 * std::max<int64_t>(KL, 1)));
+  CUDA_TRY(c.get(), cudaMemcpy(c->d_nbr, P.nbr.data(), sizeof(int) * 4 * KL, cudaMemcpyHostToDevice));
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_code, 4 * std::max<int64_t>(KL, 1)));
+  CUDA_TRY(c.get(), cudaMemcpy(c->d_code, P.code.data(), 4 * KL, cudaMemcpyHostToDevice));
+  const size_t sb = state_bytes(c.get());
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(c.get(), cudaMalloc(&c->d_Q[b], std::max<size_t>(sb, 16)));
+    CUDA_TRY(c.get(), cudaMemset(c->d_Q[b], 0, sb));
+  }
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_res, std::max<size_t>(sb, 16)));
+  CUDA_TRY(c.get(), cudaMemset(c->d_res, 0, sb));
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_flag, sizeof(int)));
+  const int64_t nghost = P.num_ghost(), nsend = P.send_off.empty() ? 0 : P.send_off.back();
+  const size_t per_face = 4 * (size_t)c->Nfp * c->rb;
+  if (nghost > 0) CUDA_TRY(c.get(), cudaMalloc(&c->d_ghost, nghost * per_face));
+  if (nsend > 0) {
+    CUDA_TRY(c.get(), cudaMalloc(&c->d_send, nsend * per_face));
+    CUDA_TRY(c.get(), cudaMalloc(&c->d_sendfaces, sizeof(int) * 2 * nsend));
+    CUDA_TRY(c.get(), cudaMemcpy(c->d_sendfaces, P.send_faces.data(), sizeof(int) * 2 * nsend, cudaMemcpyHostToDevice));
+  }
+  CUDA_TRY(c.get(), cudaDeviceSynchronize());
+  *out = c.release();
+  return BBWADG_OK;
+}
+
+bbwadg_status prepare_global(const bbwadg_mesh* mesh, int N, int M, const double* c2, const bbwadg_options* opts,
+                             int nparts, GlobalMesh& g) {
+  if (!mesh || !mesh->vertices || !mesh->elements || mesh->num_elements < 1 || mesh->num_vertices < 4 || !c2)
+    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "mesh/c2 pointers or sizes invalid");
+  if (N < 1 || N > BBWADG_MAX_N || M < 0 || M > N)
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "need 1 <= N <= 9 and 0 <= M <= N");
+  if (opts && opts->dtype != BBWADG_F64 && opts->dtype != BBWADG_F32)
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "dtype must be BBWADG_F64 or BBWADG_F32");
+  if (opts && (opts->tau_p < 0 || opts->tau_u < 0)) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "tau must be >= 0");
+  g.K = mesh->num_elements;
+  g.nv = mesh->num_vertices;
+  g.V = mesh->vertices;
+  g.EV = mesh->elements;
+  std::string e = check_orientation(g);
+  if (!e.empty()) return fail(nullptr, BBWADG_ERR_MESH, e);
+  e = build_connectivity(g);
+  if (!e.empty()) return fail(nullptr, BBWADG_ERR_MESH, e);
+  e = partition(g, nparts, opts ? opts->partition : nullptr);
+  if (!e.empty()) return fail(nullptr, BBWADG_ERR_INVALID_ARG, e);
+  return BBWADG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void bbwadg_default_options(bbwadg_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->dtype = BBWADG_F64;
+  o->tau_p = 1.0;
+  o->tau_u = 1.0;
+  o->world_size = 1;
+  o->check_c2 = 1;
+}
+
+bbwadg_status bbwadg_setup(const bbwadg_mesh* mesh, int N, int M, const double* c2_coeffs, const bbwadg_options* opts,
+                           bbwadg_ctx* out) {
+  if (!out) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  bbwadg_options o;
+  bbwadg_default_options(&o);
+  if (opts) o = *opts;
+  if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size)
+    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "rank/world_size invalid");
+  if (o.world_size > 1 && !o.nccl_unique_id)
+    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "world_size > 1 needs nccl_unique_id");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(nullptr, BBWADG_ERR_NO_DEVICE, "no CUDA device");
+  GlobalMesh g;
+  bbwadg_status s = prepare_global(mesh, N, M, c2_coeffs, &o, o.world_size, g);
+  if (s) return s;
+  s = setup_one(g, N, M, c2_coeffs, o, o.rank, o.world_size, nullptr, out);
+  if (s) return s;
+  bbwadg_ctx c = *out;
+  if (o.world_size > 1) {
+    std::string why;
+    if (!nccl::load(why)) {
+      bbwadg_destroy(c);
+      *out = nullptr;
+      return fail(nullptr, BBWADG_ERR_NCCL, why);
+    }
+    if (nccl::comm_init_rank(&c->comm, o.world_size, o.nccl_unique_id, o.rank) != 0) {
+      bbwadg_destroy(c);
+      *out = nullptr;
+      return fail(nullptr, BBWADG_ERR_NCCL, "ncclCommInitRank failed");
+    }
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  }
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_setup_group(const bbwadg_mesh* mesh, int N, int M, const double* c2_coeffs,
+                                 const bbwadg_options* opts, int nparts, bbwadg_ctx* out) {
+  if (!out || nparts < 1) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad group arguments");
+  bbwadg_options o;
+  bbwadg_default_options(&o);
+  if (opts) o = *opts;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(nullptr, BBWADG_ERR_NO_DEVICE, "no CUDA device");
+  GlobalMesh g;
+  bbwadg_status s = prepare_global(mesh, N, M, c2_coeffs, &o, nparts, g);
+  if (s) return s;
+  Group* grp = new Group();
+  cudaStream_t shared = nullptr;
+  for (int r = 0; r < nparts; ++r) {
+    bbwadg_ctx c = nullptr;
+    s = setup_one(g, N, M, c2_coeffs, o, r, nparts, shared, &c);
+    if (s) {
+      for (auto p : grp->parts) bbwadg_destroy(p);
+      delete grp;
+      return s;
+    }
+    if (r == 0) {
+      shared = c->stream;
+      grp->stream = c->own_stream ? c->stream : nullptr;
+      c->own_stream = false;
+    }
+    c->group = grp;
+    c->group_index = r;
+    grp->parts.push_back(c);
+    out[r] = c;
+  }
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_set_state(bbwadg_ctx c, const void* Q, int on_device) {
+  if (!c || !Q) return fail(c, BBWADG_ERR_INVALID_ARG, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  size_t sb = state_bytes(c);
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_Q[c->cur], Q, sb, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->d_res, 0, sb, c->stream));
+  if (!on_device) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_get_state(bbwadg_ctx c, void* Q, int on_device) {
+  if (!c || !Q) return fail(c, BBWADG_ERR_INVALID_ARG, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  CUDA_TRY(c, cudaMemcpyAsync(Q, c->d_Q[c->cur], state_bytes(c),
+                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  if (!on_device) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_set_source(bbwadg_ctx c, const double* gsrc) {
+  if (!c) return fail(c, BBWADG_ERR_INVALID_ARG, "null ctx");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->d_src) {
+    CUDA_TRY(c, cudaFree(c->d_src));
+    c->d_src = nullptr;
+  }
+  if (!gsrc) return BBWADG_OK;
+  const Part& P = c->part;
+  std::vector<double> loc((size_t)P.K_local * c->Np);
+  for (int64_t i = 0; i < P.K_local; ++i)
+    std::memcpy(&loc[(size_t)i * c->Np], gsrc + (size_t)P.gid[i] * c->Np, sizeof(double) * c->Np);
+  return upload_real(c, &c->d_src, loc);
+}
+
+bbwadg_status bbwadg_rhs(bbwadg_ctx c, const void* Q_dev, double t, void* dQdt_dev) {
+  if (!c || !Q_dev || !dQdt_dev) return fail(c, BBWADG_ERR_INVALID_ARG, "null argument");
+  if (c->group) return fail(c, BBWADG_ERR_INVALID_ARG, "bbwadg_rhs is not available on group contexts");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return full_pass(c, 1, Q_dev, dQdt_dev, 0, 0, 0, t);
+}
+
+bbwadg_status bbwadg_wadg_apply(bbwadg_ctx c, const void* r_dev, void* out_dev) {
+  if (!c || !r_dev || !out_dev) return fail(c, BBWADG_ERR_INVALID_ARG, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return launch_pass(c, 2, r_dev, out_dev, 0, c->part.K_local, 0, 0, 0, 0);
+}
+
+bbwadg_status bbwadg_step(bbwadg_ctx c, double t, double dt) {
+  if (!c) return fail(c, BBWADG_ERR_INVALID_ARG, "null ctx");
+  if (c->group) return fail(c, BBWADG_ERR_INVALID_ARG, "use bbwadg_group_step for group contexts");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  for (int s = 0; s < 5; ++s) {
+    bbwadg_status st = full_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], RK_A[s], RK_B[s], dt, t + RK_C[s] * dt);
+    if (st) return st;
+    c->cur ^= 1;
+  }
+  c->steps++;
+  c->t = t + dt;
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_group_step(bbwadg_ctx* ctxs, int n, double t, double dt) {
+  if (!ctxs || n < 1) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad group");
+  for (int s = 0; s < 5; ++s) {
+    // pack all partitions, then copy every ghost block from its owner's send buffer
+    for (int r = 0; r < n; ++r) {
+      bbwadg_ctx c = ctxs[r];
+      int64_t ns = c->part.send_off.back();
+      CUDA_TRY(c, c->ks.launch_pack(c->d_Q[c->cur], c->d_sendfaces, (int)ns, fnode_ptr(c), c->d_send, c->stream));
+    }
+    for (int r = 0; r < n; ++r) {
+      bbwadg_ctx c = ctxs[r];
+      const size_t per_face = 4 * (size_t)c->Nfp * c->rb;
+      for (int q = 0; q < n; ++q) {
+        int64_t nr = c->part.recv_off[q + 1] - c->part.recv_off[q];
+        if (nr == 0) continue;
+        bbwadg_ctx peer = ctxs[q];
+        int64_t ns = peer->part.send_off[r + 1] - peer->part.send_off[r];
+        if (ns != nr) return fail(c, BBWADG_ERR_MESH, "halo size mismatch between partitions");
+        CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->d_ghost) + c->part.recv_off[q] * per_face,
+                                    static_cast<char*>(peer->d_send) + peer->part.send_off[r] * per_face,
+                                    nr * per_face, cudaMemcpyDeviceToDevice, c->stream));
+      }
+    }
+    for (int r = 0; r < n; ++r) {
+      bbwadg_ctx c = ctxs[r];
+      const Part& P = c->part;
+      bbwadg_status st = launch_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], 0, P.n_interior, RK_A[s], RK_B[s], dt,
+                                     t + RK_C[s] * dt);
+      if (st) return st;
+      st = launch_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], P.n_interior, P.K_local, RK_A[s], RK_B[s], dt,
+                       t + RK_C[s] * dt);
+      if (st) return st;
+    }
+    for (int r = 0; r < n; ++r) ctxs[r]->cur ^= 1;
+  }
+  for (int r = 0; r < n; ++r) {
+    ctxs[r]->steps++;
+    ctxs[r]->t = t + dt;
+  }
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_run(bbwadg_ctx c, double t0, double dt, int64_t nsteps) {
+  if (!c || nsteps < 0) return fail(c, BBWADG_ERR_INVALID_ARG, "bad arguments");
+  for (int64_t i = 0; i < nsteps; ++i) {
+    bbwadg_status s = bbwadg_step(c, t0 + i * dt, dt);
+    if (s) return s;
+  }
+  CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  long long n = (long long)c->part.K_local * 4 * c->Np;
+  if (n > 0) {
+    if (c->dtype == BBWADG_F64)
+      nonfinite_kernel<double><<<592, 256, 0, c->stream>>>(static_cast<const double*>(c->d_Q[c->cur]), n, c->d_flag);
+    else
+      nonfinite_kernel<float><<<592, 256, 0, c->stream>>>(static_cast<const float*>(c->d_Q[c->cur]), n, c->d_flag);
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  int flag = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (flag) {
+    std::ostringstream os;
+    os << "non-finite state after step " << c->steps;
+    return fail(c, BBWADG_ERR_NONFINITE, os.str());
+  }
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_synchronize(bbwadg_ctx c) {
+  if (!c) return fail(c, BBWADG_ERR_INVALID_ARG, "null ctx");
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_query(bbwadg_ctx c, bbwadg_info* info) {
+  if (!c || !info) return fail(c, BBWADG_ERR_INVALID_ARG, "null argument");
+  const Part& P = c->part;
+  info->num_elements_global = c->K_global;
+  info->num_elements_local = P.K_local;
+  info->num_interior_local = P.n_interior;
+  info->num_halo_faces = P.num_ghost();
+  info->N = c->N;
+  info->M = c->M;
+  info->Np = c->Np;
+  info->Mp = c->Mp;
+  info->dtype = c->dtype;
+  info->rank = P.rank;
+  info->world_size = P.nparts;
+  info->global_ids = P.gid.data();
+  // minimum HBM traffic of one fused stage: Q_in, res (read) + Q_out, res (write) = 16 Np words,
+  // c^2_M (Mp words), geometry (12 words), connectivity (4 int32 + 4 bytes) per element.
+  const double per_elem = (16.0 * c->Np + c->Mp + 12.0) * c->rb + 20.0;
+  info->algorithmic_bytes_per_stage = per_elem * P.K_local;
+  const int N = c->N, M = c->M, Np = c->Np, Nfp = c->Nfp;
+  double vol = 24.0 * np3(N - 1) + 8.0 * Np * 4;                  // gradient (24 flop/b) + elevation (8 flop/out)
+  double surf = 4.0 * (Nfp * 20.0 + 2 * Nfp * 14.0 + 2 * 6.0 * np3(N - 1) + 16.0 * Np / 4.0 * 4.0);
+  double mult = 2.0 * Np * c->Mp + np3(N + M);
+  double proj = 0;
+  for (int n = N + 1; n <= N + M; ++n) proj += 8.0 * np3(n - 1);
+  for (int n = 1; n <= N; ++n) proj += 8.0 * np3(n - 1) + 10.0 * np3(n);
+  double lsrk = 4.0 * 4 * Np;
+  info->flops_per_stage = (vol + surf + mult + proj + lsrk) * P.K_local;
+  info->kernels_per_stage = (P.nparts > 1) ? 3 : 1;
+  info->steps_taken = c->steps;
+  info->time = c->t;
+  return BBWADG_OK;
+}
+
+const char* bbwadg_error_string(bbwadg_ctx c) { return c ? c->err.c_str() : g_last_error.c_str(); }
+const char* bbwadg_last_error(void) { return g_last_error.c_str(); }
+
+void bbwadg_destroy(bbwadg_ctx c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* bufs[] = {c->d_tab, c->d_Q[0], c->d_Q[1], c->d_res, c->d_c2, c->d_geo, c->d_nbr, c->d_code,
+                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (c->comm) nccl::comm_destroy(c->comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->group) {
+    Group* g = c->group;
+    auto it = std::find(g->parts.begin(), g->parts.end(), c);
+    if (it != g->parts.end()) g->parts.erase(it);
+    if (g->parts.empty()) {
+      if (g->stream) cudaStreamDestroy(g->stream);
+      delete g;
+    }
+  }
+  delete c;
+}
+
+bbwadg_status bbwadg_partition_plan(const bbwadg_mesh* mesh, int nparts, const int cuts[3], int rank, int64_t* sizes,
+                                    int64_t* gid, int64_t* send, int64_t* recv) {
+  if (!mesh || !mesh->vertices || !mesh->elements || nparts < 1 || rank < 0 || rank >= nparts || !sizes)
+    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad arguments");
+  GlobalMesh g;
+  g.K = mesh->num_elements;
+  g.nv = mesh->num_vertices;
+  g.V = mesh->vertices;
+  g.EV = mesh->elements;
+  std::string e = check_orientation(g);
+  if (e.empty()) e = build_connectivity(g);
+  if (!e.empty()) return fail(nullptr, BBWADG_ERR_MESH, e);
+  e = partition(g, nparts, cuts);
+  if (!e.empty()) return fail(nullptr, BBWADG_ERR_INVALID_ARG, e);
+  Part P = build_part(g, rank, nparts);
+  const int64_t ns = P.send_off.back(), ng = P.num_ghost();
+  sizes[0] = P.K_local;
+  sizes[1] = P.n_interior;
+  sizes[2] = ns;
+  sizes[3] = ng;
+  if (gid) std::copy(P.gid.begin(), P.gid.end(), gid);
+  if (send) {
+    for (int r = 0; r < nparts; ++r)
+      for (int64_t i = P.send_off[r]; i < P.send_off[r + 1]; ++i) {
+        int64_t k = P.gid[P.send_faces[2 * i]];
+        int f = P.send_faces[2 * i + 1];
+        send[4 * i] = k;
+        send[4 * i + 1] = f;
+        send[4 * i + 2] = r;
+        send[4 * i + 3] = g.etoe[4 * k + f];
+      }
+  }
+  if (recv) {
+    for (int64_t i = 0; i < P.K_local; ++i)
+      for (int f = 0; f < 4; ++f) {
+        int nb = P.nbr[4 * i + f];
+        if (nb > -2) continue;
+        int64_t slot = -2 - (int64_t)nb;
+        int src = 0;
+        while (P.recv_off[src + 1] <= slot) ++src;
+        int64_t k = P.gid[i];
+        recv[4 * slot] = k;
+        recv[4 * slot + 1] = f;
+        recv[4 * slot + 2] = src;
+        recv[4 * slot + 3] = g.etoe[4 * k + f];
+      }
+  }
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_projection_constants(int N, int M, double* out) {
+  if (!out || N < 0 || N > 30 || M < 0) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad arguments");
+  auto c = projection_constants(N, M);
+  std::copy(c.begin(), c.end(), out);
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_mass_inverse_constants(int N, double* out) {
+  if (!out || N < 0 || N > 30) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad arguments");
+  auto c = mass_inverse_constants(N);
+  std::copy(c.begin(), c.end(), out);
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_nccl_unique_id(void* out) {
+  if (!out) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "null out");
+  std::string why;
+  if (!nccl::load(why)) return fail(nullptr, BBWADG_ERR_NCCL, why);
+  if (nccl::get_unique_id(out) != 0) return fail(nullptr, BBWADG_ERR_NCCL, "ncclGetUniqueId failed");
+  return BBWADG_OK;
+}
+
+// Debug/test hook (not in the public header): copy the host table blob of (N, M, fp_bytes).
+// offsets[0..11] = byte offsets (up, dn, dec, fnode, nbrvol, nbrface, triup, l0, lgather, invfactN,
+// invfactM, post); returns the blob size, copies min(size, cap) bytes into out when out != NULL.
+int64_t bbwadg_debug_tables(int N, int M, int fp_bytes, void* out, int64_t cap, int64_t* offsets, double* cj,
+                            double* lj) {
+  HostTables T;
+  try {
+    T = build_tables(N, M, fp_bytes);
+  } catch (...) {
+    return -1;
+  }
+  if (offsets) {
+    size_t o[12] = {T.off_up, T.off_dn, T.off_dec, T.off_fnode, T.off_nbrvol, T.off_nbrface,
+                    T.off_triup, T.off_l0, T.off_lgather, T.off_invfactN, T.off_invfactM, T.off_post};
+    for (int i = 0; i < 12; ++i) offsets[i] = (int64_t)o[i];
+  }
+  if (cj)
+    for (int j = 0; j <= N; ++j) cj[j] = T.cj[j];
+  if (lj)
+    for (int j = 0; j <= N; ++j) lj[j] = T.lj[j];
+  if (out) std::memcpy(out, T.blob.data(), std::min<size_t>(T.blob.size(), (size_t)cap));
+  return (int64_t)T.blob.size();
+}
+
+const char* bbwadg_version(void) { return "bbwadg-b200 0.1 (sm_100a, fused stage kernel v1)"; }
+
+}  // extern "C"

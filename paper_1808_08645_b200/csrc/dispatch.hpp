@@ -1,0 +1,32 @@
+// Registry of the compiled (N, M, dtype) kernel instantiations.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bbw {
+
+struct KernelSet {
+  // args points to StageArgs<double> or StageArgs<float>
+  cudaError_t (*launch_stage)(const void* args, int grid, cudaStream_t s) = nullptr;
+  cudaError_t (*launch_pack)(const void* Q, const int* faces, int nfaces, const uint16_t* fnode, void* buf,
+                             cudaStream_t s) = nullptr;
+  cudaError_t (*prepare)() = nullptr;  // set smem attributes
+  int (*blocks_per_sm)() = nullptr;
+  int smem_bytes = 0, elems_per_cta = 0, threads = 0;
+};
+
+KernelSet get_kernels(int N, int M, int dtype);
+
+#define BBW_DECLARE_N(n) KernelSet get_kernels_N##n(int M, int dtype);
+BBW_DECLARE_N(1)
+BBW_DECLARE_N(2)
+BBW_DECLARE_N(3)
+BBW_DECLARE_N(4)
+BBW_DECLARE_N(5)
+BBW_DECLARE_N(6)
+BBW_DECLARE_N(7)
+BBW_DECLARE_N(8)
+BBW_DECLARE_N(9)
+#undef BBW_DECLARE_N
+
+}  // namespace bbw

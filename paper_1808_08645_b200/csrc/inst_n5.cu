@@ -1,0 +1,3 @@
+// Kernel instantiations for N = 5, all M in 0..N, fp64 and fp32.
+#include "instantiate.cuh"
+BBW_INSTANTIATE(5)

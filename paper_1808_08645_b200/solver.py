@@ -1,0 +1,122 @@
+"""User-facing wrapper over the C ABI (PyTorch provides device memory and streams).
+
+    from paper_1808_08645_b200 import Solver
+    s = Solver(vertices, elements, N=7, M=4, c2=c2M)        # c2M: [K, Np(M)] float64
+    s.set_state(Q0)                                        # numpy [K,4,Np] or CUDA tensor
+    s.run(t0=0.0, dt=dt, nsteps=100)
+    Q = s.get_state()                                      # numpy, global element order
+
+No arithmetic of the method happens here: every call forwards to libbbwadg.so.
+"""
+from __future__ import annotations
+
+from math import comb
+
+import numpy as np
+
+from . import lib as L
+
+
+class Solver:
+    def __init__(self, vertices, elements, N: int, M: int, c2, *, dtype: str = "f64", tau_p: float = 1.0,
+                 tau_u: float = 1.0, device: int = 0, stream=None, rank: int = 0, world_size: int = 1,
+                 nccl_id: bytes | None = None, partition=None, check_c2: bool = True):
+        import torch
+
+        self.torch = torch
+        self.N, self.M = int(N), int(M)
+        self.Np, self.Mp = comb(N + 3, 3), comb(M + 3, 3)
+        self.dtype = dtype
+        self.tdtype = torch.float64 if dtype == "f64" else torch.float32
+        self.device = torch.device("cuda", device)
+        self._v = np.ascontiguousarray(vertices, dtype=np.float64)
+        self._e = np.ascontiguousarray(elements, dtype=np.int64)
+        c2 = np.ascontiguousarray(c2, dtype=np.float64)
+        if c2.shape != (self._e.shape[0], self.Mp):
+            raise ValueError(f"c2 must have shape [K, {self.Mp}]")
+        o = L.bbwadg_default_options()
+        o.dtype = L.BBWADG_F64 if dtype == "f64" else L.BBWADG_F32
+        o.tau_p, o.tau_u, o.device = float(tau_p), float(tau_u), int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        self.stream = stream
+        o.rank, o.world_size = int(rank), int(world_size)
+        self._nccl_id = None
+        if world_size > 1:
+            if nccl_id is None:
+                raise ValueError("world_size > 1 needs the NCCL unique id (bbwadg_nccl_unique_id on rank 0)")
+            import ctypes
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_unique_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
+        if partition is not None:
+            for i in range(3):
+                o.partition[i] = int(partition[i])
+        o.check_c2 = 1 if check_c2 else 0
+        self.ctx = L.bbwadg_setup(self._v, self._e, self.N, self.M, c2, o)
+        info = self.info()
+        self.K_local = info["num_elements_local"]
+        self.global_ids = info["global_ids"]
+
+    # -------------------------------------------------------------------------------- state
+    def _host_dtype(self):
+        return np.float64 if self.dtype == "f64" else np.float32
+
+    def set_state(self, Q):
+        """Q: numpy [K_global,4,Np] (global order) or a CUDA tensor [K_local,4,Np] (local order)."""
+        if isinstance(Q, np.ndarray):
+            if Q.shape[0] != self.K_local:
+                Q = Q[self.global_ids]
+            Q = np.ascontiguousarray(Q, dtype=self._host_dtype())
+            L.bbwadg_set_state(self.ctx, Q, 0)
+        else:
+            L.bbwadg_set_state(self.ctx, Q.contiguous(), 1)
+
+    def get_state(self, device: bool = False):
+        if device:
+            out = self.torch.empty((self.K_local, 4, self.Np), dtype=self.tdtype, device=self.device)
+            L.bbwadg_get_state(self.ctx, out, 1)
+            return out
+        out = np.empty((self.K_local, 4, self.Np), dtype=self._host_dtype())
+        L.bbwadg_get_state(self.ctx, out, 0)
+        return out
+
+    def set_source(self, g):
+        L.bbwadg_set_source(self.ctx, None if g is None else np.ascontiguousarray(g, dtype=np.float64))
+
+    # -------------------------------------------------------------------------------- compute
+    def rhs(self, Q_dev, t: float = 0.0):
+        out = self.torch.empty_like(Q_dev)
+        L.bbwadg_rhs(self.ctx, Q_dev.contiguous(), t, out)
+        return out
+
+    def wadg_apply(self, r_dev):
+        out = self.torch.empty_like(r_dev)
+        L.bbwadg_wadg_apply(self.ctx, r_dev.contiguous(), out)
+        return out
+
+    def step(self, t: float, dt: float):
+        L.bbwadg_step(self.ctx, t, dt)
+
+    def run(self, t0: float, dt: float, nsteps: int):
+        L.bbwadg_run(self.ctx, t0, dt, nsteps)
+
+    def synchronize(self):
+        L.bbwadg_synchronize(self.ctx)
+
+    def info(self) -> dict:
+        i = L.bbwadg_query(self.ctx)
+        d = {f: getattr(i, f) for f, _ in L.bbwadg_info._fields_ if f != "global_ids"}
+        d["global_ids"] = np.ctypeslib.as_array(i.global_ids, shape=(i.num_elements_local,)).copy()
+        return d
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            L.bbwadg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,270 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star):
+  fp64: relative L2 error <= 1e-12 per RHS / WADG apply, <= 1e-10 after 100 steps;
+  fp32: relative L2 error <= 1e-5.
+Inputs: seeded random coefficients (rng 1808), random c^2 Bernstein coefficients in
+[0.5, 1.5] (rng 808), Kuhn meshes; sizes span several CTA batches plus a ragged tail.
+"""
+import numpy as np
+import pytest
+
+from oracle.acoustic import AcousticOracle
+from workloads import kuhn, media, states
+
+pytestmark = pytest.mark.gpu
+
+# (N, M) cases: every N with M = 0, 1, N//2+1 and N (deduplicated), plus the BASELINE configs
+CASES = sorted({(N, M) for N in range(1, 10) for M in (0, 1, N // 2 + 1, N) if M <= N} | {(5, 3), (7, 4)})
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+def _solver(v, e, N, M, c2, **kw):
+    from paper_1808_08645_b200 import Solver
+
+    return Solver(v, e, N, M, c2, **kw)
+
+
+@pytest.fixture(scope="module")
+def mesh3():
+    return kuhn.kuhn_mesh(3)  # K = 162
+
+
+@pytest.mark.parametrize("N,M", CASES)
+def test_wadg_apply_parity(gpu_lib, mesh3, N, M):
+    import torch
+
+    v, e = mesh3
+    c2 = media.random_c2(len(e), M)
+    r = np.random.default_rng(7).standard_normal((len(e), states.num_coeffs(N)))
+    o = AcousticOracle(v, e, N, M, c2)
+    s = _solver(v, e, N, M, c2)
+    out = s.wadg_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    ref = o.wadg(r)
+    assert rel_l2(out, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("N,M", CASES)
+def test_rhs_parity(gpu_lib, mesh3, N, M):
+    import torch
+
+    v, e = mesh3
+    c2 = media.random_c2(len(e), M)
+    Q = states.random_state(len(e), N)
+    o = AcousticOracle(v, e, N, M, c2, tau_p=1.0, tau_u=1.0)
+    s = _solver(v, e, N, M, c2)
+    out = s.rhs(torch.from_numpy(Q).cuda(), 0.0).cpu().numpy()
+    ref = o.rhs(Q)
+    err = rel_l2(out, ref)
+    assert err <= 1e-12, err
+
+
+@pytest.mark.parametrize("tau", [(0.0, 0.0), (0.3, 2.0)])
+def test_rhs_parity_penalties(gpu_lib, mesh3, tau):
+    import torch
+
+    v, e = mesh3
+    N, M = 4, 2
+    c2 = media.random_c2(len(e), M)
+    Q = states.random_state(len(e), N)
+    o = AcousticOracle(v, e, N, M, c2, tau_p=tau[0], tau_u=tau[1])
+    s = _solver(v, e, N, M, c2, tau_p=tau[0], tau_u=tau[1])
+    out = s.rhs(torch.from_numpy(Q).cuda(), 0.0).cpu().numpy()
+    assert rel_l2(out, o.rhs(Q)) <= 1e-12
+
+
+def test_rhs_with_source(gpu_lib, mesh3):
+    import torch
+
+    v, e = mesh3
+    N, M = 3, 2
+    f = media.c2_smooth(1.0)
+    c2 = media.project_c2(v, e, f, M)
+    g = states.manufactured_source(v, e, N, f)
+    Q = states.random_state(len(e), N)
+    o = AcousticOracle(v, e, N, M, c2, source=g)
+    s = _solver(v, e, N, M, c2)
+    s.set_source(g)
+    t = 0.37
+    out = s.rhs(torch.from_numpy(Q).cuda(), t).cpu().numpy()
+    assert rel_l2(out, o.rhs(Q, t)) <= 1e-12
+
+
+def test_config1_100_steps(gpu_lib):
+    # BASELINE config 1: 48 tets, N=3, M=1, smooth c^2; extended to 100 steps (north_star: <= 1e-10)
+    v, e = kuhn.kuhn_mesh(2)
+    N, M = 3, 1
+    c2 = media.project_c2(v, e, media.c2_smooth(1.0), M)
+    Q0 = states.random_state(len(e), N)
+    dt = 0.5 * kuhn.min_height(v, e) / (np.sqrt(c2.max()) * (N + 1) ** 2)
+    o = AcousticOracle(v, e, N, M, c2)
+    ref = o.run(Q0, 0.0, dt, 100)
+    s = _solver(v, e, N, M, c2)
+    s.set_state(Q0)
+    s.run(0.0, dt, 100)
+    out = s.get_state()
+    assert rel_l2(out, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("N,M", [(1, 1), (5, 3), (7, 4), (9, 9)])
+def test_steps_parity(gpu_lib, N, M):
+    v, e = kuhn.kuhn_mesh(2)
+    c2 = media.random_c2(len(e), M)
+    Q0 = states.random_state(len(e), N)
+    dt = 0.5 * kuhn.min_height(v, e) / (np.sqrt(1.5) * (N + 1) ** 2)
+    nsteps = 10
+    ref = AcousticOracle(v, e, N, M, c2).run(Q0, 0.0, dt, nsteps)
+    s = _solver(v, e, N, M, c2)
+    s.set_state(Q0)
+    s.run(0.0, dt, nsteps)
+    assert rel_l2(s.get_state(), ref) <= 1e-11
+
+
+@pytest.mark.parametrize("N,M", [(5, 3), (3, 1), (7, 4)])
+def test_fp32_rhs(gpu_lib, N, M):
+    import torch
+
+    # BASELINE config 4 variant: fp32 parity <= 1e-5 (layered media on the n=8 mesh for (5,3))
+    n = 8 if (N, M) == (5, 3) else 3
+    v, e = kuhn.kuhn_mesh(n)
+    c2 = media.project_c2(v, e, media.c2_layered(), M) if (N, M) == (5, 3) else media.random_c2(len(e), M)
+    Q = states.random_state(len(e), N)
+    ref = AcousticOracle(v, e, N, M, c2).rhs(Q)
+    s = _solver(v, e, N, M, c2, dtype="f32")
+    out = s.rhs(torch.from_numpy(Q.astype(np.float32)).cuda(), 0.0).cpu().numpy().astype(np.float64)
+    assert rel_l2(out, ref) <= 1e-5
+
+
+def test_fp32_steps(gpu_lib):
+    v, e = kuhn.kuhn_mesh(8)
+    N, M = 5, 3
+    c2 = media.project_c2(v, e, media.c2_layered(), M)
+    Q0 = states.gaussian_pulse(v, e, N, width=10.0)
+    dt = 0.5 * kuhn.min_height(v, e) / (np.sqrt(2.25) * (N + 1) ** 2)
+    ref = AcousticOracle(v, e, N, M, c2).run(Q0, 0.0, dt, 5)
+    s = _solver(v, e, N, M, c2, dtype="f32")
+    s.set_state(Q0)
+    s.run(0.0, dt, 5)
+    assert rel_l2(s.get_state().astype(np.float64), ref) <= 1e-5
+
+
+# ------------------------------------------------------------------------------------ edge cases
+def test_single_element(gpu_lib):
+    import torch
+
+    v = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    e = np.array([[0, 1, 2, 3]])
+    for N, M in [(1, 0), (4, 2), (9, 9)]:
+        c2 = media.random_c2(1, M)
+        Q = states.random_state(1, N)
+        ref = AcousticOracle(v, e, N, M, c2).rhs(Q)
+        out = _solver(v, e, N, M, c2).rhs(torch.from_numpy(Q).cuda(), 0.0).cpu().numpy()
+        assert rel_l2(out, ref) <= 1e-12
+
+
+def test_distorted_unstructured_mesh(gpu_lib):
+    import torch
+
+    # perturb interior vertices of a Kuhn mesh (still positively oriented): general affine tets,
+    # all 6 face orientations exercised
+    v, e = kuhn.kuhn_mesh(3)
+    rng = np.random.default_rng(3)
+    inner = np.all(np.abs(v) < 1 - 1e-9, axis=1)
+    v = v.copy()
+    v[inner] += 0.04 * rng.uniform(-1, 1, size=(inner.sum(), 3))
+    # random relabelling of local vertices, keeping positive orientation
+    e = e.copy()
+    for k in range(len(e)):
+        p = rng.permutation(4)
+        ek = e[k, p]
+        X = v[ek]
+        if np.linalg.det(np.stack([X[1] - X[0], X[2] - X[0], X[3] - X[0]])) < 0:
+            ek[[2, 3]] = ek[[3, 2]]
+        e[k] = ek
+    N, M = 4, 2
+    c2 = media.random_c2(len(e), M)
+    Q = states.random_state(len(e), N)
+    ref = AcousticOracle(v, e, N, M, c2).rhs(Q)
+    out = _solver(v, e, N, M, c2).rhs(torch.from_numpy(Q).cuda(), 0.0).cpu().numpy()
+    assert rel_l2(out, ref) <= 1e-12
+
+
+def test_constant_state_steady(gpu_lib, mesh3):
+    import torch
+
+    # p = 0, u = const: no jumps anywhere (u+ = u on the boundary) -> dQ/dt = 0 exactly
+    v, e = mesh3
+    N, M = 5, 2
+    Q = np.zeros((len(e), 4, states.num_coeffs(N)))
+    Q[:, 1], Q[:, 2], Q[:, 3] = 0.3, -1.2, 2.0
+    out = _solver(v, e, N, M, media.random_c2(len(e), M)).rhs(torch.from_numpy(Q).cuda(), 0.0).cpu().numpy()
+    assert np.max(np.abs(out)) < 1e-12
+
+
+def test_errors_are_loud(gpu_lib):
+    from paper_1808_08645_b200.lib import BBWADGError
+
+    v, e = kuhn.kuhn_mesh(1)
+    with pytest.raises(BBWADGError):  # unsupported degree
+        _solver(v, e, 10, 1, np.ones((len(e), 4)))
+    bad = e.copy()
+    bad[0, [2, 3]] = bad[0, [3, 2]]  # negative orientation
+    with pytest.raises(BBWADGError, match="MESH"):
+        _solver(v, bad, 2, 1, np.ones((len(e), 4)))
+    c2 = np.ones((len(e), 4))
+    c2[3] = -1.0
+    with pytest.raises(BBWADGError, match="NONPOSITIVE_C2"):
+        _solver(v, e, 2, 1, c2)
+
+
+def test_nonfinite_detection(gpu_lib):
+    from paper_1808_08645_b200.lib import BBWADGError
+
+    v, e = kuhn.kuhn_mesh(1)
+    N, M = 2, 1
+    s = _solver(v, e, N, M, np.ones((len(e), 4)))
+    Q = states.random_state(len(e), N)
+    Q[2, 0, 3] = np.nan
+    s.set_state(Q)
+    with pytest.raises(BBWADGError, match="NONFINITE"):
+        s.run(0.0, 1e-3, 1)
+
+
+# ------------------------------------------------------------------------------------ partitions
+@pytest.mark.parametrize("nparts", [2, 4, 8])
+def test_group_partition_bitwise(gpu_lib, nparts):
+    """P in-process partitions with device-copy halos == 1 partition, bitwise."""
+    from paper_1808_08645_b200 import lib as L
+
+    v, e = kuhn.kuhn_mesh(4)
+    N, M = 4, 2
+    c2 = media.random_c2(len(e), M)
+    Q0 = states.random_state(len(e), N)
+    dt = 1e-3
+    single = _solver(v, e, N, M, c2)
+    single.set_state(Q0)
+    for i in range(3):
+        single.step(i * dt, dt)
+    ref = single.get_state()
+    o = L.bbwadg_default_options()
+    ctxs = L.bbwadg_setup_group(v, e, N, M, c2, o, nparts)
+    gids = []
+    for c in ctxs:
+        info = L.bbwadg_query(c)
+        g = np.ctypeslib.as_array(info.global_ids, shape=(info.num_elements_local,)).copy()
+        gids.append(g)
+        L.bbwadg_set_state(c, np.ascontiguousarray(Q0[g]), 0)
+        assert info.num_halo_faces > 0
+    for i in range(3):
+        L.bbwadg_group_step(ctxs, i * dt, dt)
+    out = np.zeros_like(ref)
+    for c, g in zip(ctxs, gids):
+        loc = np.empty((len(g), 4, states.num_coeffs(N)))
+        L.bbwadg_get_state(c, loc, 0)
+        out[g] = loc
+    for c in ctxs:
+        L.bbwadg_destroy(c)
+    assert np.array_equal(out, ref)

@@ -61,13 +61,28 @@ def _fit_operator(n: int, q: int):
 
 
 def l2_fit(vertices: np.ndarray, elements: np.ndarray, func, degree: int, extra: int = 4,
-           chunk: int = 65536) -> np.ndarray:
+           chunk: int = 65536, device=None) -> np.ndarray:
     """Bernstein coefficients [K, Np(degree)] of the per-element L2 projection
-    of ``func(x, y, z)`` (vectorised) onto P^degree, canonical index order."""
+    of ``func(x, y, z)`` (vectorised; numpy or torch ufuncs via ``xp=``) onto
+    P^degree, canonical index order.  ``device="cuda"`` evaluates with torch
+    (fp64) on the GPU -- input synthesis for million-element meshes only."""
     q = degree + extra
     lam, P = _fit_operator(degree, q)
     K = elements.shape[0]
     out = np.empty((K, P.shape[0]), dtype=np.float64)
+    if device is not None:
+        import torch
+
+        lam_t = torch.from_numpy(lam).to(device)
+        P_t = torch.from_numpy(P).to(device)
+        V_t = torch.from_numpy(vertices).to(device)
+        chunk = max(1024, int(6e7 // lam.shape[0]))  # ~0.5 GB of fp64 points per chunk
+        for s in range(0, K, chunk):
+            E_t = torch.from_numpy(elements[s:s + chunk]).to(device)
+            pts = torch.einsum("qv,cvd->cqd", lam_t, V_t[E_t])
+            fv = func(pts[..., 0], pts[..., 1], pts[..., 2], xp=torch)
+            out[s:s + chunk] = (fv @ P_t.T).cpu().numpy()
+        return out
     for s in range(0, K, chunk):
         X = vertices[elements[s:s + chunk]]  # c,4,3
         pts = np.einsum("qv,cvd->cqd", lam, X)

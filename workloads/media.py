@@ -21,22 +21,22 @@ PARITY_C2_SEED = 808
 
 
 def c2_smooth(k: float = 1.0):
-    def f(x, y, z):
-        return 1.0 + 0.5 * np.sin(k * np.pi * x) * np.sin(k * np.pi * y) * np.sin(k * np.pi * z)
+    def f(x, y, z, xp=np):
+        return 1.0 + 0.5 * xp.sin(k * np.pi * x) * xp.sin(k * np.pi * y) * xp.sin(k * np.pi * z)
     return f
 
 
 def c2_layered(z0: float = -0.3, z1: float = 0.35, values=(1.0, 1.5, 2.25)):
-    def f(x, y, z):
-        return np.where(z < z0, values[0], np.where(z < z1, values[1], values[2])) + 0.0 * x
+    def f(x, y, z, xp=np):
+        return xp.where(z < z0, values[0], xp.where(z < z1, values[1], values[2])) + 0.0 * x
     return f
 
 
-def project_c2(vertices, elements, func, M: int) -> np.ndarray:
+def project_c2(vertices, elements, func, M: int, device=None) -> np.ndarray:
     """c^2_M: per-element L2 projection onto P^M (P:286 'quadrature-based L2
-    projection'), with a rule exact to degree 2(M+2)+... (q = M+4 points per
-    direction; R16 uses q = N+M+2 >= M+4 for the positivity check)."""
-    return l2_fit(vertices, elements, func, M, extra=4)
+    projection') with q = M+4 points per direction (exact for polynomial
+    integrands of degree 2M+7)."""
+    return l2_fit(vertices, elements, func, M, extra=4, device=device)
 
 
 def random_c2(K: int, M: int, seed: int = PARITY_C2_SEED, lo: float = 0.5, hi: float = 1.5) -> np.ndarray:
