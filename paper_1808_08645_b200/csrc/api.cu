@@ -246,42 +246,53 @@ bbwadg_status upload_real(bbwadg_ctx c, void** dst, const std::vector<double>& h
   return BBWADG_OK;
 }
 
-// c^2_M at the vertices and at interior sample points (R16): Bernstein evaluation by
-// de Casteljau-free direct formula in long double.
-bool c2_positive(const double* c2, int M, std::string& why, int64_t k) {
-  // sample: vertices + a barycentric lattice of degree M+2
-  int q = M + 2;
-  auto idx = indices3(M);
-  for (int b3 = 0; b3 <= q; ++b3)
-    for (int b2 = 0; b2 <= q - b3; ++b2)
-      for (int b1 = 0; b1 <= q - b3 - b2; ++b1) {
-        long double lam[4] = {(long double)(q - b1 - b2 - b3) / q, (long double)b1 / q, (long double)b2 / q,
-                              (long double)b3 / q};
-        long double v = 0;
-        for (size_t i = 0; i < idx.size(); ++i) {
-          long double term = 1;
-          int fac = 1;
-          for (int m = 2; m <= M; ++m) fac *= m;
-          long double mult = fac;
-          for (int j = 0; j < 4; ++j) {
-            for (int m = 2; m <= idx[i].a[j]; ++m) mult /= m;
-            for (int p = 0; p < idx[i].a[j]; ++p) term *= lam[j];
+// c^2_M positivity check (R16): values at the degree-(M+2) barycentric lattice of
+// each element (includes the 4 vertices); basis values precomputed once.
+struct C2Checker {
+  int M = 0, npts = 0, mp = 0;
+  std::vector<double> B;  // [npts][mp]
+  explicit C2Checker(int M_) : M(M_) {
+    int q = M + 2;
+    auto idx = indices3(M);
+    mp = (int)idx.size();
+    for (int b3 = 0; b3 <= q; ++b3)
+      for (int b2 = 0; b2 <= q - b3; ++b2)
+        for (int b1 = 0; b1 <= q - b3 - b2; ++b1) {
+          long double lam[4] = {(long double)(q - b1 - b2 - b3) / q, (long double)b1 / q, (long double)b2 / q,
+                                (long double)b3 / q};
+          for (int i = 0; i < mp; ++i) {
+            long double mult = 1, term = 1;
+            for (int m = 2; m <= M; ++m) mult *= m;
+            for (int j = 0; j < 4; ++j) {
+              for (int m = 2; m <= idx[i].a[j]; ++m) mult /= m;
+              for (int p = 0; p < idx[i].a[j]; ++p) term *= lam[j];
+            }
+            B.push_back((double)(mult * term));
           }
-          v += mult * term * c2[i];
+          ++npts;
         }
-        if (!(v > 0)) {
-          std::ostringstream os;
-          os << "c^2_M is not positive in element " << k << " (value " << (double)v << ")";
-          why = os.str();
-          return false;
-        }
-      }
-  return true;
-}
+  }
+  // returns the minimum sampled value
+  double min_value(const double* c) const {
+    double mn = 1e300;
+    for (int p = 0; p < npts; ++p) {
+      double v = 0;
+      for (int i = 0; i < mp; ++i) v += B[(size_t)p * mp + i] * c[i];
+      mn = v < mn ? v : mn;
+    }
+    return mn;
+  }
+};
 
 bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, const bbwadg_options& o, int rank,
                         int nparts, cudaStream_t shared_stream, bbwadg_ctx* out) {
   std::unique_ptr<bbwadg_ctx_s> c(new bbwadg_ctx_s());
+  struct Cleanup {  // release device resources on every early-error return
+    std::unique_ptr<bbwadg_ctx_s>& p;
+    ~Cleanup() {
+      if (p) bbwadg_destroy(p.release());
+    }
+  } cleanup{c};
   c->N = N;
   c->M = M;
   c->dtype = o.dtype;
@@ -317,17 +328,31 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   // per-element inputs in local order
   const int64_t KL = P.K_local;
   std::vector<double> geo(12 * KL), c2l((size_t)KL * c->Mp);
+  C2Checker chk(M);
+  int64_t bad = -1;
+  double badv = 0;
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < KL; ++i) {
     element_gradients(g, P.gid[i], &geo[12 * i]);
-    std::memcpy(&c2l[(size_t)i * c->Mp], c2 + (size_t)P.gid[i] * c->Mp, sizeof(double) * c->Mp);
+    const double* ci = c2 + (size_t)P.gid[i] * c->Mp;
+    std::memcpy(&c2l[(size_t)i * c->Mp], ci, sizeof(double) * c->Mp);
     if (o.check_c2) {
-      std::string why;
-      if (!c2_positive(c2 + (size_t)P.gid[i] * c->Mp, M, why, P.gid[i])) {
-        bbwadg_ctx raw = c.release();
-        bbwadg_destroy(raw);
-        return fail(nullptr, BBWADG_ERR_NONPOSITIVE_C2, why);
+      double mn = chk.min_value(ci);
+      if (!(mn > 0)) {
+#pragma omp critical
+        {
+          if (bad < 0 || P.gid[i] < bad) {
+            bad = P.gid[i];
+            badv = mn;
+          }
+        }
       }
     }
+  }
+  if (bad >= 0) {
+    std::ostringstream os;
+    os << "c^2_M is not positive in element " << bad << " (sampled value " << badv << ")";
+    return fail(nullptr, BBWADG_ERR_NONPOSITIVE_C2, os.str());
   }
   bbwadg_status s;
   if ((s = upload_real(c.get(), &c->d_geo, geo))) return fail(nullptr, s, c->err);
