@@ -16,6 +16,7 @@
 #include "nccl_shim.hpp"
 #include "stage_kernel.cuh"
 #include "tables.hpp"
+#include "layout.hpp"
 
 using namespace bbw;
 
@@ -119,15 +120,11 @@ void fill_args(bbwadg_ctx c, StageArgs<R>& a) {
   a.src = static_cast<const R*>(c->d_src);
   a.tab = static_cast<const uint8_t*>(c->d_tab);
   const HostTables& T = c->tables;
-  a.off = TableOffsets{(uint32_t)T.off_up,     (uint32_t)T.off_dn,      (uint32_t)T.off_dec,
-                       (uint32_t)T.off_fnode,  (uint32_t)T.off_nbrvol,  (uint32_t)T.off_nbrface,
-                       (uint32_t)T.off_triup,  (uint32_t)T.off_l0,      (uint32_t)T.off_lgather,
-                       (uint32_t)T.off_invfactN, (uint32_t)T.off_invfactM, (uint32_t)T.off_post};
   a.tau_p = (R)c->tau_p;
   a.tau_u = (R)c->tau_u;
   for (int j = 0; j < 10; ++j) {
-    a.cj[j] = (R)T.cj[j];
-    a.lj[j] = (R)T.lj[j];
+    a.gam[j] = (R)T.gam[j];
+    a.lam[j] = (R)T.lam[j];
   }
 }
 
@@ -172,7 +169,8 @@ bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, i
 }
 
 const uint16_t* fnode_ptr(bbwadg_ctx c) {
-  return reinterpret_cast<const uint16_t*>(static_cast<const uint8_t*>(c->d_tab) + c->tables.off_fnode);
+  const TabLayout L = tab_layout(c->N, c->M, (int)c->rb);
+  return reinterpret_cast<const uint16_t*>(static_cast<const uint8_t*>(c->d_tab) + L.fnode);
 }
 
 // NCCL halo for source state Q: pack on the comm stream, grouped send/recv, event.
@@ -763,23 +761,17 @@ bbwadg_status bbwadg_nccl_unique_id(void* out) {
 // Debug/test hook (not in the public header): copy the host table blob of (N, M, fp_bytes).
 // offsets[0..11] = byte offsets (up, dn, dec, fnode, nbrvol, nbrface, triup, l0, lgather, invfactN,
 // invfactM, post); returns the blob size, copies min(size, cap) bytes into out when out != NULL.
-int64_t bbwadg_debug_tables(int N, int M, int fp_bytes, void* out, int64_t cap, int64_t* offsets, double* cj,
-                            double* lj) {
+int64_t bbwadg_debug_tables(int N, int M, int fp_bytes, void* out, int64_t cap, double* gam, double* lam) {
   HostTables T;
   try {
     T = build_tables(N, M, fp_bytes);
   } catch (...) {
     return -1;
   }
-  if (offsets) {
-    size_t o[12] = {T.off_up, T.off_dn, T.off_dec, T.off_fnode, T.off_nbrvol, T.off_nbrface,
-                    T.off_triup, T.off_l0, T.off_lgather, T.off_invfactN, T.off_invfactM, T.off_post};
-    for (int i = 0; i < 12; ++i) offsets[i] = (int64_t)o[i];
-  }
-  if (cj)
-    for (int j = 0; j <= N; ++j) cj[j] = T.cj[j];
-  if (lj)
-    for (int j = 0; j <= N; ++j) lj[j] = T.lj[j];
+  if (gam)
+    for (int j = 0; j <= N; ++j) gam[j] = T.gam[j];
+  if (lam)
+    for (int j = 0; j <= N; ++j) lam[j] = T.lam[j];
   if (out) std::memcpy(out, T.blob.data(), std::min<size_t>(T.blob.size(), (size_t)cap));
   return (int64_t)T.blob.size();
 }

@@ -1,5 +1,6 @@
 // Host-side tables for the fast Bernstein path.  See tables.hpp for the formulas.
 #include "tables.hpp"
+#include "layout.hpp"
 
 #include <cmath>
 #include <cstring>
@@ -45,88 +46,126 @@ std::vector<double> mass_inverse_constants(int N) {
 }
 
 namespace {
-struct Blob {
-  std::vector<uint8_t> b;
-  size_t reserve(size_t bytes) {
-    size_t off = (b.size() + 15) & ~size_t(15);
-    b.resize(off + bytes, 0);
-    return off;
-  }
-  template <class T>
-  T* at(size_t off) { return reinterpret_cast<T*>(b.data() + off); }
-};
-
 long double prodfact(const int* a, int n) {
   long double p = 1.0L;
   for (int i = 0; i < n; ++i) p *= lfact(a[i]);
   return p;
 }
-
-template <class R>
-void put_real(Blob& B, size_t off, int i, long double v) {
-  R x = (R)v;
-  std::memcpy(B.b.data() + off + i * sizeof(R), &x, sizeof(R));
-}
+struct Writer {
+  std::vector<uint8_t>& b;
+  template <class T>
+  void put(int off, int i, T v) { std::memcpy(b.data() + off + (size_t)i * sizeof(T), &v, sizeof(T)); }
+  void real(int off, int i, long double v, int RB) {
+    if (RB == 8) put<double>(off, i, (double)v);
+    else put<float>(off, i, (float)v);
+  }
+  void u16x4(int off, int i, const int o[4]) {
+    for (int j = 0; j < 4; ++j) {
+      if (o[j] < 0 || o[j] > 0xFFFF) throw std::runtime_error("table offset out of 16-bit range");
+      put<uint16_t>(off, 4 * i + j, (uint16_t)o[j]);
+    }
+  }
+};
 }  // namespace
 
-HostTables build_tables(int N, int M, int fp_bytes) {
+HostTables build_tables(int N, int M, int RB) {
   if (N < 1 || N > 9 || M < 0 || M > N) throw std::runtime_error("unsupported (N, M)");
   HostTables T;
   T.N = N;
   T.M = M;
-  Blob B;
-  const int NP = np3(N), NFP = np2(N), MP = np3(M), NPH = np3(N + M);
+  T.RB = RB;
+  const TabLayout L = tab_layout(N, M, RB);
+  T.blob.assign(L.total, 0);
+  Writer W{T.blob};
+  const int NFP = np2(N);
 
-  // --- up[n][beta] (n = 0..N+M-1): ranks in degree n+1 of beta + e_j, exponents of beta
-  T.off_up = B.reserve(sizeof(uint64_t) * np4(N + M - 1));
-  for (int n = 0; n < N + M; ++n) {
-    auto idx = indices3(n);
-    uint64_t* dst = B.at<uint64_t>(T.off_up) + np4(n - 1);
+  // VG: volume gradient, b in degree N-1 -> rank_N(b + e_i)
+  {
+    auto idx = indices3(N - 1);
     for (size_t i = 0; i < idx.size(); ++i) {
       const int* a = idx[i].a;
-      int r[4] = {rank3(n + 1, a[1], a[2], a[3]), rank3(n + 1, a[1] + 1, a[2], a[3]),
-                  rank3(n + 1, a[1], a[2] + 1, a[3]), rank3(n + 1, a[1], a[2], a[3] + 1)};
-      dst[i] = pack_ranks4(r, a);
+      int o[4] = {rank3(N, a[1], a[2], a[3]) * RB, rank3(N, a[1] + 1, a[2], a[3]) * RB,
+                  rank3(N, a[1], a[2] + 1, a[3]) * RB, rank3(N, a[1], a[2], a[3] + 1) * RB};
+      W.u16x4(L.vg, (int)i, o);
     }
   }
-  // --- dn[n][alpha] (n = 0..N): ranks in degree n-1 of alpha - e_j (0 when alpha_j == 0)
-  T.off_dn = B.reserve(sizeof(uint64_t) * np4(N));
-  for (int n = 0; n <= N; ++n) {
-    auto idx = indices3(n);
-    uint64_t* dst = B.at<uint64_t>(T.off_dn) + np4(n - 1);
+  // VE: volume elevation, a in degree N -> (rank_{N-1}(a - e_j) + 1) * RB, 0 = zero slot
+  auto elev_offsets = [&](int n, const int* a, int o[4]) {
+    int d[4][3] = {{a[1], a[2], a[3]}, {a[1] - 1, a[2], a[3]}, {a[1], a[2] - 1, a[3]}, {a[1], a[2], a[3] - 1}};
+    for (int j = 0; j < 4; ++j) o[j] = a[j] > 0 ? (rank3(n - 1, d[j][0], d[j][1], d[j][2]) + 1) * RB : 0;
+  };
+  {
+    auto idx = indices3(N);
+    for (size_t i = 0; i < idx.size(); ++i) {
+      int o[4];
+      elev_offsets(N, idx[i].a, o);
+      W.u16x4(L.ve, (int)i, o);
+    }
+  }
+  // RED: degree n -> n-1, b in degree n-1 -> rank_n(b + e_j) * RB
+  for (int n = 1; n <= N + M; ++n) {
+    auto idx = indices3(n - 1);
     for (size_t i = 0; i < idx.size(); ++i) {
       const int* a = idx[i].a;
-      int r[4] = {0, 0, 0, 0};
-      if (n > 0) {
-        if (a[0] > 0) r[0] = rank3(n - 1, a[1], a[2], a[3]);
-        if (a[1] > 0) r[1] = rank3(n - 1, a[1] - 1, a[2], a[3]);
-        if (a[2] > 0) r[2] = rank3(n - 1, a[1], a[2] - 1, a[3]);
-        if (a[3] > 0) r[3] = rank3(n - 1, a[1], a[2], a[3] - 1);
+      int o[4] = {rank3(n, a[1], a[2], a[3]) * RB, rank3(n, a[1] + 1, a[2], a[3]) * RB,
+                  rank3(n, a[1], a[2] + 1, a[3]) * RB, rank3(n, a[1], a[2], a[3] + 1) * RB};
+      W.u16x4(L.red, red_off(n) + (int)i, o);
+    }
+  }
+  // UPW: degree n-1 -> n elevation with level weight 1/(a!)^2 (16-byte entries)
+  for (int n = 1; n <= N; ++n) {
+    auto idx = indices3(n);
+    for (size_t i = 0; i < idx.size(); ++i) {
+      int o[4];
+      elev_offsets(n, idx[i].a, o);
+      const int e = upw_off(n) + (int)i;
+      for (int j = 0; j < 4; ++j) W.put<uint16_t>(L.upw + 16 * e, j, (uint16_t)o[j]);
+      long double f = prodfact(idx[i].a, 4);
+      W.real(L.upw + 16 * e + 8, 0, 1.0L / (f * f), RB);
+    }
+  }
+  // LG: lift gather, per volume node and face: byte offset of (layer a_f, face-restricted index)
+  {
+    auto idx = indices3(N);
+    for (size_t i = 0; i < idx.size(); ++i) {
+      const int* a = idx[i].a;
+      for (int f = 0; f < 4; ++f) {
+        int j = a[f];
+        int c[3];
+        for (int s = 0; s < 3; ++s) c[s] = a[FACE_V[f][s]];
+        int li = (layer_off(N, j) + rank2(N - j, c[1], c[2])) * RB;
+        if (li > 0xFFFF) throw std::runtime_error("lift offset overflow");
+        W.put<uint16_t>(L.lg + 16 * (int)i, f, (uint16_t)li);
+        W.put<uint8_t>(L.lg + 16 * (int)i + 8, f, (uint8_t)j);
       }
-      dst[i] = pack_ranks4(r, a);
     }
   }
-  // --- dec[n][i] (n = 0..N+M): exponents packed 5 bits each
-  T.off_dec = B.reserve(sizeof(uint32_t) * np4(N + M));
-  for (int n = 0; n <= N + M; ++n) {
-    auto idx = indices3(n);
-    uint32_t* dst = B.at<uint32_t>(T.off_dec) + np4(n - 1);
-    for (size_t i = 0; i < idx.size(); ++i) {
-      const int* a = idx[i].a;
-      dst[i] = (uint32_t)(a[0] | (a[1] << 5) | (a[2] << 10) | (a[3] << 15));
+  // TRIRED: face degree m+1 -> m, c in degree m -> trirank_{m+1}(c + e_s) * RB
+  for (int m = 0; m < N; ++m) {
+    auto tm = indices2(m);
+    for (size_t i = 0; i < tm.size(); ++i) {
+      const int* c = tm[i].c;
+      int o[4] = {rank2(m + 1, c[1], c[2]) * RB, rank2(m + 1, c[1] + 1, c[2]) * RB, rank2(m + 1, c[1], c[2] + 1) * RB,
+                  0};
+      W.u16x4(L.trired, trired_off(m) + (int)i, o);
     }
   }
-  // --- face tables
+  // TRIELE: face degree N-1 -> N, c in degree N -> (trirank_{N-1}(c - e_s) + 1) * RB or 0
   auto tri = indices2(N);
-  T.off_fnode = B.reserve(sizeof(uint16_t) * 4 * NFP);
+  for (int i = 0; i < NFP; ++i) {
+    const int* c = tri[i].c;
+    int o[4] = {c[0] > 0 ? (rank2(N - 1, c[1], c[2]) + 1) * RB : 0,
+                c[1] > 0 ? (rank2(N - 1, c[1] - 1, c[2]) + 1) * RB : 0,
+                c[2] > 0 ? (rank2(N - 1, c[1], c[2] - 1) + 1) * RB : 0, 0};
+    W.u16x4(L.triele, i, o);
+  }
+  // face node maps
   for (int f = 0; f < 4; ++f)
     for (int i = 0; i < NFP; ++i) {
       int a[4] = {0, 0, 0, 0};
       for (int s = 0; s < 3; ++s) a[FACE_V[f][s]] = tri[i].c[s];
-      B.at<uint16_t>(T.off_fnode)[f * NFP + i] = (uint16_t)rank3(N, a[1], a[2], a[3]);
+      W.put<uint16_t>(L.fnode, f * NFP + i, (uint16_t)(rank3(N, a[1], a[2], a[3]) * RB));
     }
-  T.off_nbrvol = B.reserve(sizeof(uint16_t) * 24 * NFP);
-  T.off_nbrface = B.reserve(sizeof(uint16_t) * 6 * NFP);
   for (int fp = 0; fp < 4; ++fp)
     for (int sg = 0; sg < 6; ++sg)
       for (int i = 0; i < NFP; ++i) {
@@ -134,90 +173,59 @@ HostTables build_tables(int N, int M, int fp_bytes) {
         for (int s = 0; s < 3; ++s) d[PERM[sg][s]] = tri[i].c[s];
         int a[4] = {0, 0, 0, 0};
         for (int t = 0; t < 3; ++t) a[FACE_V[fp][t]] = d[t];
-        B.at<uint16_t>(T.off_nbrvol)[(fp * 6 + sg) * NFP + i] = (uint16_t)rank3(N, a[1], a[2], a[3]);
-        if (fp == 0) B.at<uint16_t>(T.off_nbrface)[sg * NFP + i] = (uint16_t)rank2(N, d[1], d[2]);
+        W.put<uint16_t>(L.nbrvol, (fp * 6 + sg) * NFP + i, (uint16_t)rank3(N, a[1], a[2], a[3]));
+        if (fp == 0) W.put<uint16_t>(L.nbrface, sg * NFP + i, (uint16_t)rank2(N, d[1], d[2]));
       }
-  // --- triangle reductions: triup[m][c] (m = 0..N-1): ranks in degree m+1 of c + e_s
-  T.off_triup = B.reserve(sizeof(uint64_t) * np3(N - 1));
-  for (int m = 0; m < N; ++m) {
-    auto tm = indices2(m);
-    uint64_t* dst = B.at<uint64_t>(T.off_triup) + np3(m - 1);
-    for (size_t i = 0; i < tm.size(); ++i) {
-      const int* c = tm[i].c;
-      int r0 = rank2(m + 1, c[1], c[2]), r1 = rank2(m + 1, c[1] + 1, c[2]), r2 = rank2(m + 1, c[1], c[2] + 1);
-      uint64_t v = (uint64_t)r0 | ((uint64_t)r1 << 8) | ((uint64_t)r2 << 16);
-      v |= ((uint64_t)c[0] << 24) | ((uint64_t)c[1] << 29) | ((uint64_t)c[2] << 34);
-      dst[i] = v;
-    }
-  }
-  // --- L_0 7-point stencil on the face (degree N): neighbours c - e_a + e_b
-  T.off_l0 = B.reserve(sizeof(uint64_t) * NFP);
-  for (int i = 0; i < NFP; ++i) {
-    const int* c = tri[i].c;
-    uint64_t v = 0;
-    for (int p = 0; p < 6; ++p) {
-      int a = L0_PAIRS[p][0], b = L0_PAIRS[p][1];
-      int nbi = i;
-      if (c[a] > 0) {
-        int d[3] = {c[0], c[1], c[2]};
-        d[a] -= 1;
-        d[b] += 1;
-        nbi = rank2(N, d[1], d[2]);
-      }
-      v |= (uint64_t)nbi << (8 * p);
-    }
-    v |= ((uint64_t)c[0] << 48) | ((uint64_t)c[1] << 53) | ((uint64_t)c[2] << 58);
-    B.at<uint64_t>(T.off_l0)[i] = v;
-  }
-  // --- lift gather: for volume alpha and face f, index into the (face, flux) layer buffer
-  T.off_lgather = B.reserve(sizeof(uint32_t) * NP);
-  {
-    auto idx = indices3(N);
-    for (int i = 0; i < NP; ++i) {
-      const int* a = idx[i].a;
-      uint32_t v = 0;
-      for (int f = 0; f < 4; ++f) {
-        int j = a[f];
-        int off = 0;
-        for (int jj = 0; jj < j; ++jj) off += np2(N - jj);
-        int c[3];
-        for (int s = 0; s < 3; ++s) c[s] = a[FACE_V[f][s]];
-        int li = off + rank2(N - j, c[1], c[2]);
-        v |= (uint32_t)li << (8 * f);
-      }
-      B.at<uint32_t>(T.off_lgather)[i] = v;
-    }
-  }
-  // --- factorial scalings of the Bernstein product (Eq. mcoeff):
-  //     h_g = [g! N! M!/(N+M)!] sum_b (r_{g-b}/(g-b)!) (c_b/b!)
-  T.off_invfactN = B.reserve(fp_bytes * NP);
-  T.off_invfactM = B.reserve(fp_bytes * MP);
-  T.off_post = B.reserve(fp_bytes * NPH);
+  // CSR of the Bernstein product (Eq. mcoeff): for g in degree N+M, all (a, b) with a + b = g
   {
     auto iN = indices3(N), iM = indices3(M), iH = indices3(N + M);
+    int t = 0;
+    for (size_t gi = 0; gi < iH.size(); ++gi) {
+      W.put<int32_t>(L.csr_ptr, (int)gi, t);
+      const int* g = iH[gi].a;
+      for (size_t bi = 0; bi < iM.size(); ++bi) {
+        const int* b = iM[bi].a;
+        if (b[0] > g[0] || b[1] > g[1] || b[2] > g[2] || b[3] > g[3]) continue;
+        int ar = rank3(N, g[1] - b[1], g[2] - b[2], g[3] - b[3]);
+        W.put<uint32_t>(L.csr_terms, t++, (uint32_t)(ar * RB) | ((uint32_t)(bi * RB) << 16));
+      }
+    }
+    W.put<int32_t>(L.csr_ptr, (int)iH.size(), t);
+    if (t != lnp3(N) * lnp3(M)) throw std::runtime_error("CSR term count mismatch");
+  }
+  // scale arrays
+  {
+    auto iN = indices3(N), iM = indices3(M), iH = indices3(N + M), iN1 = indices3(N - 1);
     const long double binv = lfact(N) * lfact(M) / lfact(N + M);
-    for (int i = 0; i < NP; ++i) {
-      long double v = 1.0L / prodfact(iN[i].a, 4);
-      fp_bytes == 8 ? put_real<double>(B, T.off_invfactN, i, v) : put_real<float>(B, T.off_invfactN, i, v);
+    for (int i = 0; i < (int)iN.size(); ++i) {
+      long double f = prodfact(iN[i].a, 4);
+      W.real(L.s_invfacN, i, 1.0L / f, RB);
+      W.real(L.s_facN, i, f, RB);
+      W.real(L.s_invfac2N, i, 1.0L / (f * f), RB);
+      W.real(L.s_outN, i, f / lfact(N), RB);
     }
-    for (int i = 0; i < MP; ++i) {
-      long double v = 1.0L / prodfact(iM[i].a, 4);
-      fp_bytes == 8 ? put_real<double>(B, T.off_invfactM, i, v) : put_real<float>(B, T.off_invfactM, i, v);
+    for (int i = 0; i < (int)iM.size(); ++i) W.real(L.s_invfacM, i, 1.0L / prodfact(iM[i].a, 4), RB);
+    for (int i = 0; i < (int)iH.size(); ++i) {
+      long double f = prodfact(iH[i].a, 4);
+      W.real(L.s_post, i, f * f * binv, RB);
     }
-    for (int i = 0; i < NPH; ++i) {
-      long double v = prodfact(iH[i].a, 4) * binv;
-      fp_bytes == 8 ? put_real<double>(B, T.off_post, i, v) : put_real<float>(B, T.off_post, i, v);
+    for (int i = 0; i < (int)iN1.size(); ++i) W.real(L.s_invfacNm1, i, 1.0L / prodfact(iN1[i].a, 4), RB);
+    auto t1 = indices2(N - 1);
+    for (int i = 0; i < NFP; ++i) {
+      long double f = prodfact(tri[i].c, 3);
+      W.real(L.s_cfac, i, f, RB);
+      W.real(L.s_cf2, i, f * f, RB);
+    }
+    for (int i = 0; i < (int)t1.size(); ++i) {
+      long double f = prodfact(t1[i].c, 3);
+      W.real(L.s_invf2, i, 1.0L / (f * f), RB);
     }
   }
-  B.reserve(16);
-  T.blob = std::move(B.b);
-
   auto c = projection_constants(N, M);
   for (int j = 0; j <= N; ++j) {
     T.cj[j] = c[j];
-    // lift layer constants l_j = (-1)^j C(N,j)/(j+1)
-    long double binom = lfact(N) / (lfact(j) * lfact(N - j));
-    T.lj[j] = (double)(((j & 1) ? -1.0L : 1.0L) * binom / (long double)(j + 1));
+    T.gam[j] = (double)(lfact(j) * lfact(j) * (long double)c[N - j] / lfact(N + M));
+    T.lam[j] = ((j & 1) ? -1.0 : 1.0) / (double)(j + 1);
   }
   return T;
 }

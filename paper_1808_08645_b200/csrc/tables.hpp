@@ -57,20 +57,21 @@ inline uint64_t pack_ranks4(const int r[4], const int e[4]) {
   return v;
 }
 
-// Byte image of all tables for one (N, M); offsets are in bytes from the start.
+// Byte image of all tables for one (N, M, RB) in the layout of layout.hpp, plus the
+// per-(N,M) scalar constants passed as kernel parameters.
 struct HostTables {
-  int N = 0, M = 0;
+  int N = 0, M = 0, RB = 8;
   std::vector<uint8_t> blob;
-  size_t off_up = 0, off_dn = 0, off_dec = 0, off_fnode = 0, off_nbrvol = 0, off_nbrface = 0, off_triup = 0,
-         off_l0 = 0, off_lgather = 0, off_invfactN = 0, off_invfactM = 0, off_post = 0;
-  std::array<double, 10> cj{}, lj{};
+  std::array<double, 10> cj{};   // projection constants c_0..c_N (Thm main)
+  std::array<double, 10> gam{};  // upward-sweep level constants (n!)^2 c_{N-n} / (N+M)!, n = 0..N
+  std::array<double, 10> lam{};  // lift layer constants (-1)^j/(j+1)  (= l_j / C(N,j))
 };
 
-// c_j for P^{N+M}_N (or, with M < 0, for M^-1 of the reference tetrahedron).
+// c_j for P^{N+M}_N and for M^-1 of the reference tetrahedron.
 std::vector<double> projection_constants(int N, int M);
 std::vector<double> mass_inverse_constants(int N);
 
-// Build every table for (N, M); fp_bytes = sizeof(real) of the device path.
-HostTables build_tables(int N, int M, int fp_bytes);
+// Build every table for (N, M); RB = sizeof(real) of the device path.
+HostTables build_tables(int N, int M, int RB);
 
 }  // namespace bbw
