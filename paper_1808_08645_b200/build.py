@@ -18,8 +18,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
-LIBDIR = os.path.join(HERE, "native")
+# BBWADG_VARIANT=<name> + BBWADG_DEFS="-DBBW_T=128 ..." build a tuning variant into native/<name>/
+VARIANT = os.environ.get("BBWADG_VARIANT", "")
+EXTRA_DEFS = os.environ.get("BBWADG_DEFS", "").split()
+BUILD = os.path.join(HERE, "build", VARIANT) if VARIANT else os.path.join(HERE, "build")
+LIBDIR = os.path.join(HERE, "native", VARIANT) if VARIANT else os.path.join(HERE, "native")
 LIB = os.path.join(LIBDIR, "libbbwadg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -41,9 +44,9 @@ def _compile(src: str, hdr_mtime: float, verbose: bool) -> str:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA_DEFS, "-c", src, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [NVCC, "-x", "cu", *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, "-x", "cu", *ARCH, *FLAGS, *EXTRA_DEFS, "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

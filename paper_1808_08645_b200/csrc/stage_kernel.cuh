@@ -61,10 +61,16 @@ struct StageCfg {
   static constexpr int NP = cnp3(N), NFP = cnp2(N), NFP1 = cnp2(N - 1), MP = cnp3(M), NPH = cnp3(N + M);
   static constexpr int NPM1 = cnp3(N - 1), NP4 = cnp4(N);
   static constexpr int RB = (int)sizeof(R);
-  static constexpr int T = 256;
+#ifndef BBW_T
+#define BBW_T 256
+#endif
+#ifndef BBW_SMEM_KB
+#define BBW_SMEM_KB 110
+#endif
+  static constexpr int T = BBW_T;
   static constexpr int VEC = 16 / RB;
   // ---- per-element shared-memory layout (in reals)
-  static constexpr int O_Q = 0, O_R = 4 * NP, O_GEO = 8 * NP, O_C = O_GEO + 32;
+  static constexpr int O_Q = 0, O_R = 4 * NP, O_RS = 8 * NP, O_GEO = 12 * NP, O_C = O_GEO + 32;
   static constexpr int O_W = rup(O_C + MP, 2);
   // surface phase
   static constexpr int S_G = O_W;                      // 4 x [zero, NPM1]
@@ -79,14 +85,25 @@ struct StageCfg {
   static constexpr int PER_E = rup(cmax(S_END, W_END), VEC);
   static constexpr int EB = PER_E * RB;  // element stride in bytes
   // ---- batching
+#ifdef BBW_ET
+  static constexpr int ET = BBW_ET;
+#else
   static constexpr int ET = (N <= 3) ? 4 : 2;  // elements per thread (share one table lookup)
-  static constexpr int SMEM_TARGET = 110 * 1024;
-  static constexpr int G = cmin(32, pow2_floor(cmax(1, SMEM_TARGET / (ET * EB))));
+#endif
+  static constexpr int SMEM_TARGET = BBW_SMEM_KB * 1024;
+  static constexpr int G = cmin(T / 8, pow2_floor(cmax(1, SMEM_TARGET / (ET * EB))));
   static constexpr int E = G * ET;
   static constexpr int TG = T / G;
   static constexpr int SMEM_BYTES = E * EB;
   static_assert(TG >= 8, "too many groups");
 };
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <typename R>
 __device__ __forceinline__ R ld(const char* p) { return *reinterpret_cast<const R*>(p); }
@@ -105,6 +122,7 @@ __device__ __forceinline__ void static_for(F&& f) {
 //   dst[i] = SCALE(i) * sum_j src[off_j(i)]   for the ET elements of the thread's group
 template <class C, typename R, int CNT, int SRC, int DST, int NTERMS>
 __device__ __forceinline__ void sum_phase(char* gb, int q, const ushort4* __restrict__ tab) {
+#pragma unroll 2
   for (int i = q; i < CNT; i += C::TG) {
     const ushort4 o = __ldg(tab + i);
     const char* p0 = gb + o.x;
@@ -137,6 +155,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
     R acc[ET];
 #pragma unroll
     for (int u = 0; u < ET; ++u) acc[u] = R(0);
+#pragma unroll 4
     for (int t = t0; t < t1; ++t) {
       const uint32_t w = __ldg(csr + t);
       const char* pa = gb + (w & 0xFFFF) + C::O_R * RB;
@@ -248,7 +267,17 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
     const int nE = (int)((A.elem_end - e0) < E ? (A.elem_end - e0) : E);
     const long long k0 = e0 + grp * ET;  // first element of this thread's group
 
-    // ---- A: loads
+    // ---- A: loads.  The LSRK residual of the batch is prefetched asynchronously (cp.async,
+    //      waited for before phase E) so its HBM latency overlaps the surface/volume phases.
+    if (A.mode == 0) {
+      constexpr int NV = 4 * NP / VEC;
+      const char* gr = reinterpret_cast<const char*>(A.res + e0 * 4 * NP);
+      for (int t = tid; t < nE * NV; t += T) {
+        const int e = t / NV, w = t - e * NV;
+        cp_async16(smem + e * EB + C::O_RS * RB + w * 16, gr + (size_t)t * 16);
+      }
+      cp_async_commit();
+    }
     if (A.mode == 2) {
       for (int t = tid; t < nE * NP; t += T) {
         const int e = t / NP, a = t - e * NP;
@@ -433,6 +462,10 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
         __syncthreads();
       });
       // ---- E: gather lifts; r''_p += S_p/(a!)^2 (+ source); r_u = a! r''_u + S_u/a!; LSRK for u
+      if (A.mode == 0) {
+        cp_async_wait_all();
+        __syncthreads();
+      }
       {
         R nrm[ET][12];
 #pragma unroll
@@ -474,7 +507,7 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
               for (int d = 0; d < 3; ++d) {
                 const long long gi = k * 4 * NP + (1 + d) * NP + a;
                 if (A.mode == 0) {
-                  const R rs = fma(A.rk_a, A.res[gi], A.dt * ru[d]);
+                  const R rs = fma(A.rk_a, ld<R>(eb + (C::O_RS + (1 + d) * NP + a) * RB), A.dt * ru[d]);
                   A.res[gi] = rs;
                   A.Qout[gi] = fma(A.rk_b, rs, ld<R>(eb + (C::O_Q + (1 + d) * NP + a) * RB));
                 } else {
@@ -505,7 +538,7 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
         } else {
           const long long gi = k * 4 * NP + a;
           if (A.mode == 0) {
-            const R rs = fma(A.rk_a, A.res[gi], A.dt * dp);
+            const R rs = fma(A.rk_a, ld<R>(gb + u * EB + (C::O_RS + a) * RB), A.dt * dp);
             A.res[gi] = rs;
             A.Qout[gi] = fma(A.rk_b, rs, ld<R>(gb + u * EB + (C::O_Q + a) * RB));
           } else {
