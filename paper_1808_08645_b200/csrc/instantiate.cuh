@@ -40,7 +40,7 @@ struct Inst {
     k.prepare = &prepare;
     k.blocks_per_sm = &blocks;
     k.smem_bytes = C::SMEM_BYTES;
-    k.elems_per_cta = C::E;
+    k.elems_per_cta = C::G * C::ET;
     k.threads = C::T;
     return k;
   }

@@ -1,24 +1,29 @@
-// Fused BBWADG RK-stage kernel for sm_100a, v2 (templated on N, M and the real type).
+// Fused BBWADG RK-stage kernel for sm_100a, v3 (templated on N, M, the real type and the
+// group shape).
 //
-// One persistent CTA processes batches of E = G x ET consecutive elements (Morton order, so
-// neighbour traces are mostly L2-resident).  The CTA's threads form G groups; a thread of group
-// g computes output coefficient i of a phase for the ET elements g*ET .. g*ET+ET-1 at once, so
-// each table lookup (neighbour byte offsets) is shared by ET elements and every shared-memory
-// address is "table register + compile-time immediate" (array base + element stride).
+// Work decomposition.  A CTA of T threads is split into G independent GROUPS of TG threads
+// (TG a multiple of 32).  Each group processes batches of ET consecutive elements (Morton order:
+// neighbour traces are mostly L2-resident) and synchronises only with itself (named barrier
+// `bar.sync 1+g, TG`, or __syncwarp when TG == 32), so the latency chains of different groups
+// overlap.  Within a group, thread q "owns" canonical coefficients a = q + TG k: its copies of
+// Q_in, of the LSRK residual and of r_u live in REGISTERS (the residual is loaded at batch start
+// and only consumed at the end, hiding its HBM latency); shared memory only holds the arrays
+// that stencils gather from, with the surface and WADG work regions aliased.
 //
-// All one-degree Bernstein reductions/elevations run as UNWEIGHTED 4-point sums in factorial-
-// scaled variables (layout.hpp), with the 1/n and c_j factors folded into per-level constants:
-//   A  load Q_in (16-B vectors), c^2_M / beta!, grad(lambda) and face normals
-//   B  surface fluxes F_p, F_u scaled by |grad lambda_f| c!;
-//      degree-(N-1) gradient g''_b = sum_i grad(lambda_i) q_{b+e_i} / b!
-//   C  volume r''_a = -sum_j g''_{a-e_j} (elevation, x/a! scaling); L_0 F as
-//      reduction -> 1/(d!)^2 -> elevation -> (c!)^2
-//   D  N face reductions -> lift layers w_j
-//   E  gather the 4 lifts into r; LSRK update of u_x, u_y, u_z (streamed to HBM)
-//   F  Bernstein product h'_g = (g!)^2 N!M!/(N+M)! sum r''_a c''_b  (Eq. mcoeff)
-//   G  M reductions N+M -> N;  H  N downward reductions;  I  N upward elevations with the
-//      level constants gam_n = (n!)^2 c_{N-n}/(N+M)!  (telescoping form, Eq. telescope)
-//   J  dp/dt_a = a!/N! b_N[a];  LSRK update of p
+// Per-output index work is amortised: a thread computes output i of a phase for its group's ET
+// elements (and, on faces, for all 8 face/flux arrays) from one table lookup; every shared
+// address is "table register + compile-time immediate".  One-degree Bernstein reductions and
+// elevations are UNWEIGHTED sums in factorial-scaled variables (layout.hpp).
+//   A  Q_in -> smem (16-B vectors); residual -> registers; c^2_M/b!; grad(lambda), normals
+//   B  own Q -> registers; fluxes F_p, F_u x |grad l_f| c!;
+//      g''_b = sum_i grad(l_i) q_{b+e_i} / b!                       (barycentric derivative)
+//   C  r''_a = -sum_j g''_{a-e_j} (volume); L_0 F: reduction, 1/(d!)^2, elevation, (c!)^2
+//   D  N face reductions -> lift layers
+//   E  gather the 4 lifts; LSRK update of u (registers -> HBM)
+//   F  Bernstein product h'_g = (g!)^2 N!M!/(N+M)! sum r''_a c''_b        (Eq. mcoeff)
+//   G  M reductions N+M -> N; H N downward reductions; I N upward elevations with level
+//      constants gam_n = (n!)^2 c_{N-n}/(N+M)!                        (Eq. telescope)
+//   J  dp/dt_a = a!/N! b_N[a]; LSRK update of p
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -35,7 +40,6 @@ __host__ __device__ constexpr int cnp4(int n) { return lnp4(n); }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int rup(int a, int b) { return (a + b - 1) / b * b; }
-__host__ __device__ constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1; }
 
 template <typename R>
 struct StageArgs {
@@ -55,55 +59,66 @@ struct StageArgs {
   int mode;  // 0 LSRK stage, 1 write dQ/dt into Qout, 2 WADG apply (Qin=r[K][NP] -> Qout[K][NP])
 };
 
+#ifndef BBW_T
+#define BBW_T 128
+#endif
+
+// default group shape per N: threads per group and elements per group-batch
+__host__ __device__ constexpr int default_tg(int N) { return N <= 7 ? 32 : 64; }
+__host__ __device__ constexpr int default_et(int N) { return N <= 2 ? 4 : N <= 4 ? 2 : 1; }
+#ifndef BBW_MINB
+#define BBW_MINB 4
+#endif
+
 template <int N_, int M_, typename R>
 struct StageCfg {
   static constexpr int N = N_, M = M_;
   static constexpr int NP = cnp3(N), NFP = cnp2(N), NFP1 = cnp2(N - 1), MP = cnp3(M), NPH = cnp3(N + M);
   static constexpr int NPM1 = cnp3(N - 1), NP4 = cnp4(N);
   static constexpr int RB = (int)sizeof(R);
-#ifndef BBW_T
-#define BBW_T 256
-#endif
-#ifndef BBW_SMEM_KB
-#define BBW_SMEM_KB 110
-#endif
-  static constexpr int T = BBW_T;
   static constexpr int VEC = 16 / RB;
-  // ---- per-element shared-memory layout (in reals)
-  static constexpr int O_Q = 0, O_R = 4 * NP, O_RS = 8 * NP, O_GEO = 12 * NP, O_C = O_GEO + 32;
-  static constexpr int O_W = rup(O_C + MP, 2);
-  // surface phase
-  static constexpr int S_G = O_W;                      // 4 x [zero, NPM1]
-  static constexpr int S_F = S_G + 4 * (NPM1 + 1);     // 8 x [NFP]  (face f, flux p/u)
-  static constexpr int S_Y = S_F + 8 * NFP;            // 8 x [zero, NFP1]
-  static constexpr int S_L = S_Y + 8 * (NFP1 + 1);     // 8 x [NP]   lift layers
-  static constexpr int S_END = S_L + 8 * NP;
-  // WADG phase
-  static constexpr int W_H = O_W, W_P = W_H + NPH, W_LEV = W_P + NPH;
-  static constexpr int W_A0 = W_LEV + NP4, W_A1 = W_A0 + NP + 1;
-  static constexpr int W_END = W_A1 + NP + 1;
-  static constexpr int PER_E = rup(cmax(S_END, W_END), VEC);
-  static constexpr int EB = PER_E * RB;  // element stride in bytes
-  // ---- batching
+  static constexpr int T = BBW_T;
+#ifdef BBW_TG
+  static constexpr int TG = BBW_TG;
+#else
+  static constexpr int TG = default_tg(N);
+#endif
 #ifdef BBW_ET
   static constexpr int ET = BBW_ET;
 #else
-  static constexpr int ET = (N <= 3) ? 4 : 2;  // elements per thread (share one table lookup)
+  static constexpr int ET = default_et(N);
 #endif
-  static constexpr int SMEM_TARGET = BBW_SMEM_KB * 1024;
-  static constexpr int G = cmin(T / 8, pow2_floor(cmax(1, SMEM_TARGET / (ET * EB))));
-  static constexpr int E = G * ET;
-  static constexpr int TG = T / G;
-  static constexpr int SMEM_BYTES = E * EB;
-  static_assert(TG >= 8, "too many groups");
+  static constexpr int G = T / TG;               // groups per CTA
+  static constexpr int KO = (NP + TG - 1) / TG;  // owned coefficients per thread
+  // ---- per-element shared-memory layout (in reals)
+  static constexpr int O_GEO = 0, O_C = 32, O_RP = 32 + MP;
+  static constexpr int O_X = rup(O_RP + NP, VEC);
+  static constexpr int X_Q = O_X, X_G = O_X + 4 * NP, X_L = O_X;  // Q + G'', later the lift layers
+  static constexpr int XSIZE = cmax(4 * NP + 4 * (NPM1 + 1), 8 * NP);
+  static constexpr int O_Y = O_X + XSIZE;
+  static constexpr int Y_F = O_Y, Y_Y = O_Y + 8 * NFP;  // F', Y''
+  static constexpr int YSIZE = 8 * NFP + 8 * (NFP1 + 1);
+  static constexpr int W_H = O_X, W_P = W_H + NPH, W_LEV = W_P + NPH;  // WADG (aliases X, Y)
+  static constexpr int W_A0 = W_LEV + NP4, W_A1 = W_A0 + NP + 1;
+  static constexpr int WSIZE = 2 * NPH + NP4 + 2 * (NP + 1);
+  static constexpr int PER_E = rup(O_X + cmax(XSIZE + YSIZE, WSIZE), VEC);
+  static constexpr int EB = PER_E * RB;  // element stride in bytes
+  static constexpr int GB = ET * EB;     // group stride in bytes
+  static constexpr int SMEM_BYTES = G * GB;
+  static_assert(TG % 32 == 0 && T % TG == 0 && G <= 15, "bad group shape");
 };
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+template <class C>
+struct GroupSync {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    if constexpr (C::TG == 32) {
+      __syncwarp();
+    } else {
+      asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(C::TG) : "memory");
+    }
+  }
+};
 
 template <typename R>
 __device__ __forceinline__ R ld(const char* p) { return *reinterpret_cast<const R*>(p); }
@@ -118,54 +133,128 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
-// one pure 4-point (or 3-point) sum stencil phase over CNT outputs:
-//   dst[i] = SCALE(i) * sum_j src[off_j(i)]   for the ET elements of the thread's group
-template <class C, typename R, int CNT, int SRC, int DST, int NTERMS>
-__device__ __forceinline__ void sum_phase(char* gb, int q, const ushort4* __restrict__ tab) {
-#pragma unroll 2
-  for (int i = q; i < CNT; i += C::TG) {
-    const ushort4 o = __ldg(tab + i);
-    const char* p0 = gb + o.x;
-    const char* p1 = gb + o.y;
-    const char* p2 = gb + o.z;
-    const char* p3 = gb + o.w;
+// dst[i] = sum_j src[off_j(i)] (4 terms) for the ET elements of the group.  The thread's
+// outputs i = q + TG k are fully unrolled; table loads use a clamped index so they can all be
+// issued before the shared-memory gathers (ILP), only the stores are predicated.
+template <class C, typename R, int CNT, int SRC, int DST>
+__device__ __forceinline__ void sum4_phase(char* gb, int q, const ushort4* __restrict__ tab) {
+  constexpr int K = (CNT + C::TG - 1) / C::TG;
+  ushort4 o[K];
 #pragma unroll
-    for (int u = 0; u < C::ET; ++u) {
-      constexpr int S = SRC * C::RB;
-      R v = ld<R>(p0 + S + u * C::EB) + ld<R>(p1 + S + u * C::EB) + ld<R>(p2 + S + u * C::EB);
-      if constexpr (NTERMS == 4) v += ld<R>(p3 + S + u * C::EB);
-      st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v);
+  for (int k = 0; k < K; ++k) o[k] = __ldg(tab + cmin(q + C::TG * k, CNT - 1));
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = q + C::TG * k;
+    const char* p0 = gb + o[k].x + SRC * C::RB;
+    const char* p1 = gb + o[k].y + SRC * C::RB;
+    const char* p2 = gb + o[k].z + SRC * C::RB;
+    const char* p3 = gb + o[k].w + SRC * C::RB;
+    R v[C::ET];
+#pragma unroll
+    for (int u = 0; u < C::ET; ++u)
+      v[u] = (ld<R>(p0 + u * C::EB) + ld<R>(p1 + u * C::EB)) + (ld<R>(p2 + u * C::EB) + ld<R>(p3 + u * C::EB));
+    if ((CNT % C::TG == 0) || i < CNT) {
+#pragma unroll
+      for (int u = 0; u < C::ET; ++u) st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v[u]);
     }
   }
 }
 
+// dst_ff[i] = scale(i) * sum_s src_ff[off_s(i)] (3 terms) for the 8 face/flux arrays, ET elements
+template <class C, typename R, int CNT, int SRC, int SSTRIDE, int DST, int DSTRIDE, bool SCALED>
+__device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __restrict__ tab, const R* __restrict__ scale) {
+  constexpr int K = (CNT + C::TG - 1) / C::TG;
+  ushort4 o[K];
+  R sc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int ic = cmin(q + C::TG * k, CNT - 1);
+    o[k] = __ldg(tab + ic);
+    sc[k] = SCALED ? __ldg(scale + ic) : R(1);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = q + C::TG * k;
+    if (!((CNT % C::TG == 0) || i < CNT)) continue;
+    const char* p0 = gb + o[k].x + SRC * C::RB;
+    const char* p1 = gb + o[k].y + SRC * C::RB;
+    const char* p2 = gb + o[k].z + SRC * C::RB;
+#pragma unroll
+    for (int ff = 0; ff < 8; ++ff)
+#pragma unroll
+      for (int u = 0; u < C::ET; ++u) {
+        const int so = ff * SSTRIDE * C::RB + u * C::EB;
+        R v = ld<R>(p0 + so) + ld<R>(p1 + so) + ld<R>(p2 + so);
+        if constexpr (SCALED) v *= sc[k];
+        st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, v);
+      }
+  }
+}
+
 template <class C, typename R>
-__device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A) {
+__device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync) {
   constexpr int N = C::N, M = C::M, NP = C::NP, NPH = C::NPH, RB = C::RB, ET = C::ET, EB = C::EB, TG = C::TG;
-  const TabLayout L = tab_layout(N, M, RB);
+  constexpr TabLayout L = tab_layout(N, M, RB);
   const uint8_t* tab = A.tab;
   const int* csr_ptr = reinterpret_cast<const int*>(tab + L.csr_ptr);
   const uint32_t* csr = reinterpret_cast<const uint32_t*>(tab + L.csr_terms);
   const R* post = reinterpret_cast<const R*>(tab + L.s_post);
   const ushort4* red = reinterpret_cast<const ushort4*>(tab + L.red);
 
-  // F: h'_g = post_g * sum_{a+b=g} r''_a c''_b
-  for (int g = q; g < NPH; g += TG) {
-    const int t0 = __ldg(csr_ptr + g), t1 = __ldg(csr_ptr + g + 1);
-    R acc[ET];
+  // F: h'_g = post_g * sum_{a+b=g} r''_a c''_b, output-row stationary: for output row (g2,g3) of
+  // degree N+M and every c''-row (b2,b3), the input row (g2-b2, g3-b3) of r'' is loaded once into
+  // registers and convolved (1-D, full) with the c''-row into the row accumulators.
+  {
+    constexpr int NR = cnp2(N + M), KR = (NR + TG - 1) / TG;
+    const uint32_t* rowdec = reinterpret_cast<const uint32_t*>(tab + L.rowdec);
+#pragma unroll 1
+    for (int k = 0; k < KR; ++k) {
+      const int rho = q + TG * k;
+      if (rho < NR) {
+        const uint32_t d = __ldg(rowdec + rho);
+        const int g2 = d & 0xFF, g3 = (d >> 8) & 0xFF, gs = (int)(d >> 16);
+        R acc[ET][N + M + 1];
 #pragma unroll
-    for (int u = 0; u < ET; ++u) acc[u] = R(0);
-#pragma unroll 4
-    for (int t = t0; t < t1; ++t) {
-      const uint32_t w = __ldg(csr + t);
-      const char* pa = gb + (w & 0xFFFF) + C::O_R * RB;
-      const char* pb = gb + (w >> 16) + C::O_C * RB;
+        for (int u = 0; u < ET; ++u)
 #pragma unroll
-      for (int u = 0; u < ET; ++u) acc[u] = fma(ld<R>(pa + u * EB), ld<R>(pb + u * EB), acc[u]);
+          for (int x = 0; x <= N + M; ++x) acc[u][x] = R(0);
+        static_for<0, M + 1, 1>([&](auto b3c) {
+          constexpr int b3 = decltype(b3c)::value;
+          static_for<0, M + 1 - b3, 1>([&](auto b2c) {
+            constexpr int b2 = decltype(b2c)::value;
+            constexpr int LB = M - b2 - b3 + 1;
+            constexpr int CB = cnp3(M) - cnp3(M - b3) + b2 * (2 * (M - b3) + 3 - b2) / 2;  // rank_M(0,b2,b3)
+            const int a2 = g2 - b2, a3 = g3 - b3;
+            if (a2 >= 0 && a3 >= 0 && a2 + a3 <= N) {
+              const int m = N - a3, la = m - a2 + 1;
+              const int ra = (cnp3(N) - (m + 1) * (m + 2) * (m + 3) / 6 + a2 * (2 * m + 3 - a2) / 2) * RB;
+              const char* pr = gb + C::O_RP * RB + ra;
+#pragma unroll
+              for (int u = 0; u < ET; ++u) {
+                R in[N + 1];
+#pragma unroll
+                for (int a1 = 0; a1 <= N; ++a1) in[a1] = (a1 < la) ? ld<R>(pr + a1 * RB + u * EB) : R(0);
+#pragma unroll
+                for (int b1 = 0; b1 < LB; ++b1) {
+                  const R cv = ld<R>(gb + (C::O_C + CB + b1) * RB + u * EB);
+#pragma unroll
+                  for (int a1 = 0; a1 <= N; ++a1) acc[u][a1 + b1] = fma(cv, in[a1], acc[u][a1 + b1]);
+                }
+              }
+            }
+          });
+        });
+        const int lg = N + M - g2 - g3 + 1;
+#pragma unroll
+        for (int x = 0; x <= N + M; ++x) {
+          if (x < lg) {
+            const R s = __ldg(post + gs + x);
+#pragma unroll
+            for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + gs + x) * RB + u * EB, acc[u][x] * s);
+          }
+        }
+      }
     }
-    const R s = __ldg(post + g);
-#pragma unroll
-    for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + g) * RB + u * EB, acc[u] * s);
   }
   if (q == 0) {
 #pragma unroll
@@ -174,58 +263,75 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
       st<R>(gb + C::W_A1 * RB + u * EB, R(0));
     }
   }
-  __syncthreads();
-
+  sync();
   // G: M reductions N+M -> N (ping-pong H <-> P; the last lands in level N)
   static_for<N + M, N, -1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
-    constexpr int k = N + M - n;  // iteration index
+    constexpr int k = N + M - n;
     constexpr int SRC = (k % 2 == 0) ? C::W_H : C::W_P;
     constexpr int DST = (n - 1 == N) ? C::W_LEV + cnp4(N - 1) : ((k % 2 == 0) ? C::W_P : C::W_H);
-    sum_phase<C, R, cnp3(n - 1), SRC, DST, 4>(gb, q, red + red_off(n));
-    __syncthreads();
+    sum4_phase<C, R, cnp3(n - 1), SRC, DST>(gb, q, red + red_off(n));
+    sync();
   });
   if constexpr (M == 0) {
     for (int i = q; i < NP; i += TG)
 #pragma unroll
       for (int u = 0; u < ET; ++u)
         st<R>(gb + (C::W_LEV + cnp4(N - 1) + i) * RB + u * EB, ld<R>(gb + (C::W_H + i) * RB + u * EB));
-    __syncthreads();
+    sync();
   }
-  // H: downward reductions level n -> n-1 (pure sums); seed b_0 = gam_0 u_0 in A0[1]
+  // H: downward reductions level n -> n-1
   static_for<N, 0, -1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
-    sum_phase<C, R, cnp3(n - 1), C::W_LEV + cnp4(n - 1), C::W_LEV + cnp4(n - 2), 4>(gb, q, red + red_off(n));
-    __syncthreads();
+    sum4_phase<C, R, cnp3(n - 1), C::W_LEV + cnp4(n - 1), C::W_LEV + cnp4(n - 2)>(gb, q, red + red_off(n));
+    sync();
   });
-  if (q == 0) {
-#pragma unroll
-    for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_A0 + 1) * RB + u * EB, A.gam[0] * ld<R>(gb + C::W_LEV * RB + u * EB));
-  }
-  __syncthreads();
-  // I: upward: b_n[a] = sum_j b_{n-1}[a - e_j] + gam_n / (a!)^2 u_n[a]   (b_n in A_{n%2})
+  // I: upward: b_n[a] = sum_j b_{n-1}[a - e_j] + gam_n/(a!)^2 u_n[a]   (b_n in A_{n%2}, b_0 = gam_0 u_0)
   static_for<1, N + 1, 1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
     constexpr int SRC = (n % 2 == 1) ? C::W_A0 : C::W_A1;
     constexpr int DST = (n % 2 == 1) ? C::W_A1 : C::W_A0;
     const R gn = A.gam[n];
-    const uint8_t* up = tab + L.upw + 16 * upw_off(n);
-    for (int i = q; i < cnp3(n); i += TG) {
-      const ushort4 o = __ldg(reinterpret_cast<const ushort4*>(up + 16 * i));
-      const R w = gn * __ldg(reinterpret_cast<const R*>(up + 16 * i + 8));
-      const char* p0 = gb + o.x;
-      const char* p1 = gb + o.y;
-      const char* p2 = gb + o.z;
-      const char* p3 = gb + o.w;
+    if constexpr (n == 1) {
+      // degree 1: every a has exactly one valid a - e_j (= the single b_0), weight 1/(a!)^2 = 1
+      const R g0 = A.gam[0];
+      for (int i = q; i < 4; i += TG)
 #pragma unroll
-      for (int u = 0; u < ET; ++u) {
-        constexpr int S = SRC * RB;
-        R v = (ld<R>(p0 + S + u * EB) + ld<R>(p1 + S + u * EB)) + (ld<R>(p2 + S + u * EB) + ld<R>(p3 + S + u * EB));
-        v = fma(w, ld<R>(gb + (C::W_LEV + cnp4(n - 1) + i) * RB + u * EB), v);
-        st<R>(gb + (DST + 1 + i) * RB + u * EB, v);
+        for (int u = 0; u < ET; ++u) {
+          const R b0 = g0 * ld<R>(gb + C::W_LEV * RB + u * EB);
+          st<R>(gb + (DST + 1 + i) * RB + u * EB, fma(gn, ld<R>(gb + (C::W_LEV + 1 + i) * RB + u * EB), b0));
+        }
+    } else {
+      const uint8_t* up = tab + L.upw + 16 * upw_off(n);
+      constexpr int CNT = cnp3(n), K = (CNT + TG - 1) / TG;
+      ushort4 o[K];
+      R w[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int ic = cmin(q + TG * k, CNT - 1);
+        o[k] = __ldg(reinterpret_cast<const ushort4*>(up + 16 * ic));
+        w[k] = gn * __ldg(reinterpret_cast<const R*>(up + 16 * ic + 8));
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int i = q + TG * k;
+        const char* p0 = gb + o[k].x + SRC * RB;
+        const char* p1 = gb + o[k].y + SRC * RB;
+        const char* p2 = gb + o[k].z + SRC * RB;
+        const char* p3 = gb + o[k].w + SRC * RB;
+        R v[ET];
+#pragma unroll
+        for (int u = 0; u < ET; ++u) {
+          v[u] = (ld<R>(p0 + u * EB) + ld<R>(p1 + u * EB)) + (ld<R>(p2 + u * EB) + ld<R>(p3 + u * EB));
+          v[u] = fma(w[k], ld<R>(gb + (C::W_LEV + cnp4(n - 1) + cmin(i, CNT - 1)) * RB + u * EB), v[u]);
+        }
+        if ((CNT % TG == 0) || i < CNT) {
+#pragma unroll
+          for (int u = 0; u < ET; ++u) st<R>(gb + (DST + 1 + i) * RB + u * EB, v[u]);
+        }
       }
     }
-    __syncthreads();
+    sync();
   });
 }
 
@@ -235,17 +341,18 @@ __host__ __device__ constexpr int wadg_result() {
 }
 
 template <class C, typename R>
-__global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
+__global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R> A) {
   constexpr int N = C::N, M = C::M, NP = C::NP, NFP = C::NFP, NFP1 = C::NFP1, MP = C::MP, NPM1 = C::NPM1;
-  constexpr int E = C::E, T = C::T, ET = C::ET, EB = C::EB, RB = C::RB, TG = C::TG, VEC = C::VEC;
+  constexpr int ET = C::ET, EB = C::EB, RB = C::RB, TG = C::TG, VEC = C::VEC, KO = C::KO;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ R lam_s[10];
-  char* smem = reinterpret_cast<char*>(smem_raw);
   const int tid = threadIdx.x;
-  if (tid < 10) lam_s[tid] = A.lam[tid < 9 ? tid : 9];
   const int grp = tid / TG, q = tid - grp * TG;
-  char* gb = smem + grp * ET * EB;  // this thread's group base
-  const TabLayout L = tab_layout(N, M, RB);
+  if (tid < 10) lam_s[tid] = A.lam[tid < 9 ? tid : 9];
+  __syncthreads();
+  char* gb = reinterpret_cast<char*>(smem_raw) + grp * C::GB;  // this group's elements
+  const GroupSync<C> sync{1 + grp};
+  constexpr TabLayout L = tab_layout(N, M, RB);
   const uint8_t* tab = A.tab;
   const R* invfacN = reinterpret_cast<const R*>(tab + L.s_invfacN);
   const R* facN = reinterpret_cast<const R*>(tab + L.s_facN);
@@ -254,49 +361,48 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
   const R* invfacM = reinterpret_cast<const R*>(tab + L.s_invfacM);
   const R* invfacNm1 = reinterpret_cast<const R*>(tab + L.s_invfacNm1);
   const R* cfac = reinterpret_cast<const R*>(tab + L.s_cfac);
-  const R* invf2 = reinterpret_cast<const R*>(tab + L.s_invf2);
-  const R* cf2 = reinterpret_cast<const R*>(tab + L.s_cf2);
   const uint16_t* fnode = reinterpret_cast<const uint16_t*>(tab + L.fnode);
   const uint16_t* nbrvol = reinterpret_cast<const uint16_t*>(tab + L.nbrvol);
   const uint16_t* nbrface = reinterpret_cast<const uint16_t*>(tab + L.nbrface);
 
   const long long nelem = A.elem_end - A.elem_begin;
-  const long long nbatch = (nelem + E - 1) / E;
-  for (long long batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
-    const long long e0 = A.elem_begin + batch * E;
-    const int nE = (int)((A.elem_end - e0) < E ? (A.elem_end - e0) : E);
-    const long long k0 = e0 + grp * ET;  // first element of this thread's group
+  const long long nbatch = (nelem + ET - 1) / ET;
+  for (long long batch = (long long)blockIdx.x * C::G + grp; batch < nbatch; batch += (long long)gridDim.x * C::G) {
+    const long long k0 = A.elem_begin + batch * ET;
+    const int nE = (int)((A.elem_end - k0) < ET ? (A.elem_end - k0) : ET);
 
-    // ---- A: loads.  The LSRK residual of the batch is prefetched asynchronously (cp.async,
-    //      waited for before phase E) so its HBM latency overlaps the surface/volume phases.
+    // ---- A: loads (residual -> registers; Q -> smem; geometry, c'' -> smem; zero slots)
+    R rs[ET][4][KO];
     if (A.mode == 0) {
-      constexpr int NV = 4 * NP / VEC;
-      const char* gr = reinterpret_cast<const char*>(A.res + e0 * 4 * NP);
-      for (int t = tid; t < nE * NV; t += T) {
-        const int e = t / NV, w = t - e * NV;
-        cp_async16(smem + e * EB + C::O_RS * RB + w * 16, gr + (size_t)t * 16);
-      }
-      cp_async_commit();
+#pragma unroll
+      for (int u = 0; u < ET; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int k = 0; k < KO; ++k) {
+            const int a = q + TG * k;
+            rs[u][c][k] = (u < nE && a < NP) ? __ldg(A.res + (k0 + u) * 4 * NP + c * NP + a) : R(0);
+          }
     }
     if (A.mode == 2) {
-      for (int t = tid; t < nE * NP; t += T) {
-        const int e = t / NP, a = t - e * NP;
-        st<R>(smem + e * EB + (C::O_R + a) * RB, A.Qin[(e0 + e) * NP + a] * __ldg(invfacN + a));
+      for (int t = q; t < nE * NP; t += TG) {
+        const int u = t / NP, a = t - u * NP;
+        st<R>(gb + u * EB + (C::O_RP + a) * RB, A.Qin[(k0 + u) * NP + a] * __ldg(invfacN + a));
       }
     } else {
       constexpr int NV = 4 * NP / VEC;
       using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
-      const V* gq = reinterpret_cast<const V*>(A.Qin + e0 * 4 * NP);
-      for (int t = tid; t < nE * NV; t += T) {
-        const int e = t / NV, w = t - e * NV;
-        *reinterpret_cast<V*>(smem + e * EB + w * 16) = gq[t];
+      const V* gq = reinterpret_cast<const V*>(A.Qin + k0 * 4 * NP);
+      for (int t = q; t < nE * NV; t += TG) {
+        const int u = t / NV, w = t - u * NV;
+        *reinterpret_cast<V*>(gb + u * EB + C::X_Q * RB + w * 16) = __ldg(gq + t);
       }
-      for (int t = tid; t < nE * 4; t += T) {  // grad lambda_f, |grad lambda_f|, outward normal
-        const int e = t >> 2, f = t & 3;
-        const R* gg = A.geo + (e0 + e) * 12 + 3 * f;
-        const R gx = gg[0], gy = gg[1], gz = gg[2];
+      for (int t = q; t < nE * 4; t += TG) {  // grad lambda_f, outward normal, |grad lambda_f|
+        const int u = t >> 2, f = t & 3;
+        const R* g = A.geo + (k0 + u) * 12 + 3 * f;
+        const R gx = __ldg(g), gy = __ldg(g + 1), gz = __ldg(g + 2);
         const R gl = sqrt(gx * gx + gy * gy + gz * gz), il = R(1) / gl;
-        char* s = smem + e * EB + C::O_GEO * RB;
+        char* s = gb + u * EB + C::O_GEO * RB;
         st<R>(s + (3 * f) * RB, gx);
         st<R>(s + (3 * f + 1) * RB, gy);
         st<R>(s + (3 * f + 2) * RB, gz);
@@ -305,19 +411,31 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
         st<R>(s + (14 + 4 * f) * RB, -gz * il);
         st<R>(s + (15 + 4 * f) * RB, gl);
       }
-      for (int t = tid; t < E * 12; t += T) {  // zero slots of G'' (4) and Y'' (8) arrays
-        const int e = t / 12, z = t - e * 12;
-        const int off = z < 4 ? C::S_G + z * (NPM1 + 1) : C::S_Y + (z - 4) * (NFP1 + 1);
-        st<R>(smem + e * EB + off * RB, R(0));
+      for (int t = q; t < ET * 12; t += TG) {  // zero slots of the G'' (4) and Y'' (8) arrays
+        const int u = t / 12, z = t - u * 12;
+        const int off = z < 4 ? C::X_G + z * (NPM1 + 1) : C::Y_Y + (z - 4) * (NFP1 + 1);
+        st<R>(gb + u * EB + off * RB, R(0));
       }
     }
-    for (int t = tid; t < nE * MP; t += T) {
-      const int e = t / MP, b = t - e * MP;
-      st<R>(smem + e * EB + (C::O_C + b) * RB, A.c2[(e0 + e) * MP + b] * __ldg(invfacM + b));
+    for (int t = q; t < nE * MP; t += TG) {
+      const int u = t / MP, b = t - u * MP;
+      st<R>(gb + u * EB + (C::O_C + b) * RB, __ldg(A.c2 + (k0 + u) * MP + b) * __ldg(invfacM + b));
     }
-    __syncthreads();
+    sync();
 
+    R qo[ET][4][KO];  // own Q_in coefficients (LSRK)
+    R ru[ET][3][KO];  // own r_u (x/a! scaled until phase E)
     if (A.mode != 2) {
+      // ---- B0: own Q -> registers
+#pragma unroll
+      for (int u = 0; u < ET; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int k = 0; k < KO; ++k) {
+            const int a = q + TG * k;
+            qo[u][c][k] = (a < NP) ? ld<R>(gb + u * EB + (C::X_Q + c * NP + a) * RB) : R(0);
+          }
       // ---- B1: fluxes, F' = |grad l_f| c! F
       for (int t = q; t < 4 * NFP; t += TG) {
         const int f = t / NFP, i = t - f * NFP;
@@ -325,12 +443,12 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
         const R cs = __ldg(cfac + i);
 #pragma unroll
         for (int u = 0; u < ET; ++u) {
-          const char* eb = gb + u * EB;
+          const char* eb = gb + u * EB + C::X_Q * RB;
           const long long k = k0 + u;
-          R pm = ld<R>(eb + own), uxm = ld<R>(eb + own + NP * RB), uym = ld<R>(eb + own + 2 * NP * RB),
-            uzm = ld<R>(eb + own + 3 * NP * RB);
+          const R pm = ld<R>(eb + own), uxm = ld<R>(eb + own + NP * RB), uym = ld<R>(eb + own + 2 * NP * RB),
+                  uzm = ld<R>(eb + own + 3 * NP * RB);
           R pp = -pm, uxp = uxm, uyp = uym, uzp = uzm;
-          if (k < A.elem_end) {
+          if (u < nE) {
             const int nb = __ldg(A.nbr + k * 4 + f);
             if (nb >= 0) {
               const int vol = __ldg(nbrvol + __ldg(A.code + k * 4 + f) * NFP + i);
@@ -348,17 +466,17 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
               uzp = gh[3 * NFP];
             }
           }
-          const char* gs = eb + (C::O_GEO + 12 + 4 * f) * RB;
+          const char* gs = gb + u * EB + (C::O_GEO + 12 + 4 * f) * RB;
           const R nx = ld<R>(gs), ny = ld<R>(gs + RB), nz = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * cs;
           const R jp = pp - pm;
           const R jun = nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
-          st<R>(gb + u * EB + (C::S_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));
-          st<R>(gb + u * EB + (C::S_F + (2 * f + 1) * NFP + i) * RB, R(0.5) * sc * (A.tau_u * jun - jp));
+          st<R>(gb + u * EB + (C::Y_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));
+          st<R>(gb + u * EB + (C::Y_F + (2 * f + 1) * NFP + i) * RB, R(0.5) * sc * (A.tau_u * jun - jp));
         }
       }
       // ---- B2: g''_b = sum_i grad(l_i) q_{b+e_i} / b!   (div u, grad p)
       {
-        R lg[ET][12];
+        R lg[ET][12];  // grad(lambda) of the group's elements, hoisted into registers
 #pragma unroll
         for (int u = 0; u < ET; ++u)
 #pragma unroll
@@ -370,19 +488,20 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
           const R sc = __ldg(invfacNm1 + b);
 #pragma unroll
           for (int u = 0; u < ET; ++u) {
-            const char* eb = gb + u * EB;
+            const char* eb = gb + u * EB + C::X_Q * RB;
             R div = R(0), gx = R(0), gy = R(0), gz = R(0);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
+              const R lx = lg[u][3 * j], ly = lg[u][3 * j + 1], lz = lg[u][3 * j + 2];
               const R pj = ld<R>(eb + off[j]);
-              gx = fma(lg[u][3 * j], pj, gx);
-              gy = fma(lg[u][3 * j + 1], pj, gy);
-              gz = fma(lg[u][3 * j + 2], pj, gz);
-              div = fma(lg[u][3 * j], ld<R>(eb + off[j] + NP * RB), div);
-              div = fma(lg[u][3 * j + 1], ld<R>(eb + off[j] + 2 * NP * RB), div);
-              div = fma(lg[u][3 * j + 2], ld<R>(eb + off[j] + 3 * NP * RB), div);
+              gx = fma(lx, pj, gx);
+              gy = fma(ly, pj, gy);
+              gz = fma(lz, pj, gz);
+              div = fma(lx, ld<R>(eb + off[j] + NP * RB), div);
+              div = fma(ly, ld<R>(eb + off[j] + 2 * NP * RB), div);
+              div = fma(lz, ld<R>(eb + off[j] + 3 * NP * RB), div);
             }
-            char* g = gb + u * EB + (C::S_G + 1 + b) * RB;
+            char* g = gb + u * EB + (C::X_G + 1 + b) * RB;
             st<R>(g, div * sc);
             st<R>(g + (NPM1 + 1) * RB, gx * sc);
             st<R>(g + 2 * (NPM1 + 1) * RB, gy * sc);
@@ -390,164 +509,158 @@ __global__ void __launch_bounds__(C::T) stage_kernel(const StageArgs<R> A) {
           }
         }
       }
-      __syncthreads();
-      // ---- C1: r''_c[a] = -sum_j g''_c[a - e_j]   (4 fields; zero slot for a_j = 0)
+      sync();
+      // ---- C1: r''_c[a] = -sum_j g''_c[a - e_j]  (p -> smem R_p, u -> registers)
       {
         const ushort4* ve = reinterpret_cast<const ushort4*>(tab + L.ve);
-        for (int a = q; a < NP; a += TG) {
-          const ushort4 o = __ldg(ve + a);
-          const char* p0 = gb + o.x;
-          const char* p1 = gb + o.y;
-          const char* p2 = gb + o.z;
-          const char* p3 = gb + o.w;
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+        for (int k = 0; k < KO; ++k) {
+          const int a = q + TG * k;
+          if (a < NP) {
+            const ushort4 o = __ldg(ve + a);
+            const char* p0 = gb + o.x + C::X_G * RB;
+            const char* p1 = gb + o.y + C::X_G * RB;
+            const char* p2 = gb + o.z + C::X_G * RB;
+            const char* p3 = gb + o.w + C::X_G * RB;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int u = 0; u < ET; ++u) {
+                const int S = c * (NPM1 + 1) * RB + u * EB;
+                const R v = (ld<R>(p0 + S) + ld<R>(p1 + S)) + (ld<R>(p2 + S) + ld<R>(p3 + S));
+                if (c == 0) st<R>(gb + u * EB + (C::O_RP + a) * RB, -v);
+                else ru[u][c - 1][k] = -v;
+              }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int u = 0; u < ET; ++u) ru[u][c][k] = R(0);
+          }
+        }
+      }
+      // ---- C2: Y''[ff][d] = (sum_s F'[ff][d + e_s]) / (d!)^2
+      face_sum3<C, R, NFP1, C::Y_F, NFP, C::Y_Y + 1, NFP1 + 1, true>(
+          gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(N - 1),
+          reinterpret_cast<const R*>(tab + L.s_invf2));
+      sync();
+      // ---- C3: layer 0: w'_0[c] = (2N+3) F'[c] + (c!)^2 sum_s Y''[c - e_s]
+      {
+        const ushort4* te = reinterpret_cast<const ushort4*>(tab + L.triele);
+        const R* cf2 = reinterpret_cast<const R*>(tab + L.s_cf2);
+        for (int c = q; c < NFP; c += TG) {
+          const ushort4 o = __ldg(te + c);
+          const R sc = __ldg(cf2 + c);
+#pragma unroll
+          for (int ff = 0; ff < 8; ++ff)
 #pragma unroll
             for (int u = 0; u < ET; ++u) {
-              constexpr int S0 = C::S_G * RB;
-              const int S = S0 + c * (NPM1 + 1) * RB + u * EB;
-              const R v = (ld<R>(p0 + S) + ld<R>(p1 + S)) + (ld<R>(p2 + S) + ld<R>(p3 + S));
-              st<R>(gb + u * EB + (C::O_R + c * NP + a) * RB, -v);
+              const char* ya = gb + (C::Y_Y + ff * (NFP1 + 1)) * RB + u * EB;
+              const R y = ld<R>(ya + o.x) + ld<R>(ya + o.y) + ld<R>(ya + o.z);
+              const R F = ld<R>(gb + u * EB + (C::Y_F + ff * NFP + c) * RB);
+              st<R>(gb + u * EB + (C::X_L + ff * NP + c) * RB, fma(sc, y, R(2 * N + 3) * F));
             }
         }
       }
-      // ---- C2: y''[d] = (sum_s F'[d + e_s]) / (d!)^2   (8 face arrays)
-      {
-        const ushort4* tr = reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(N - 1);
-        for (int t = q; t < 8 * NFP1; t += TG) {
-          const int ff = t / NFP1, d = t - ff * NFP1;
-          const ushort4 o = __ldg(tr + d);
-          const R sc = __ldg(invf2 + d);
-          const char* fa = gb + (C::S_F + ff * NFP) * RB;
-#pragma unroll
-          for (int u = 0; u < ET; ++u) {
-            const R v = ld<R>(fa + o.x + u * EB) + ld<R>(fa + o.y + u * EB) + ld<R>(fa + o.z + u * EB);
-            st<R>(gb + u * EB + (C::S_Y + ff * (NFP1 + 1) + 1 + d) * RB, v * sc);
-          }
-        }
-      }
-      __syncthreads();
-      // ---- C3: layer 0: w'_0[c] = (2N+3) F'[c] + (c!)^2 sum_s y''[c - e_s]
-      {
-        const ushort4* te = reinterpret_cast<const ushort4*>(tab + L.triele);
-        for (int t = q; t < 8 * NFP; t += TG) {
-          const int ff = t / NFP, c = t - ff * NFP;
-          const ushort4 o = __ldg(te + c);
-          const R sc = __ldg(cf2 + c);
-          const char* ya = gb + (C::S_Y + ff * (NFP1 + 1)) * RB;
-#pragma unroll
-          for (int u = 0; u < ET; ++u) {
-            const R y = ld<R>(ya + o.x + u * EB) + ld<R>(ya + o.y + u * EB) + ld<R>(ya + o.z + u * EB);
-            const R F = ld<R>(gb + u * EB + (C::S_F + ff * NFP + c) * RB);
-            st<R>(gb + u * EB + (C::S_L + ff * NP + c) * RB, fma(sc, y, R(2 * N + 3) * F));
-          }
-        }
-      }
-      __syncthreads();
+      sync();
       // ---- D: lift layers j = 1..N: w'_j[d] = sum_s w'_{j-1}[d + e_s]
       static_for<1, N + 1, 1>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
-        constexpr int m = N - j, CNT = cnp2(m);
-        const ushort4* tr = reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(m);
-        for (int t = q; t < 8 * CNT; t += TG) {
-          const int ff = t / CNT, d = t - ff * CNT;
-          const ushort4 o = __ldg(tr + d);
-          const char* la = gb + (C::S_L + ff * NP + layer_off(N, j - 1)) * RB;
-#pragma unroll
-          for (int u = 0; u < ET; ++u) {
-            const R v = ld<R>(la + o.x + u * EB) + ld<R>(la + o.y + u * EB) + ld<R>(la + o.z + u * EB);
-            st<R>(gb + u * EB + (C::S_L + ff * NP + layer_off(N, j) + d) * RB, v);
-          }
-        }
-        __syncthreads();
+        constexpr int m = N - j;
+        face_sum3<C, R, cnp2(m), C::X_L + layer_off(N, j - 1), NP, C::X_L + layer_off(N, j), NP, false>(
+            gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(m), static_cast<const R*>(nullptr));
+        sync();
       });
-      // ---- E: gather lifts; r''_p += S_p/(a!)^2 (+ source); r_u = a! r''_u + S_u/a!; LSRK for u
-      if (A.mode == 0) {
-        cp_async_wait_all();
-        __syncthreads();
-      }
+      // ---- E: gather lifts; r''_p += S_p/(a!)^2 (+ source) -> smem; r_u = a! r''_u + S_u/a!; LSRK for u
       {
-        R nrm[ET][12];
+        R nrm[ET][12];  // outward normals of the group's elements, hoisted into registers
 #pragma unroll
         for (int u = 0; u < ET; ++u)
 #pragma unroll
           for (int f = 0; f < 4; ++f)
 #pragma unroll
-            for (int d = 0; d < 3; ++d) nrm[u][3 * f + d] = ld<R>(gb + u * EB + (C::O_GEO + 12 + 4 * f + d) * RB);
+            for (int dd = 0; dd < 3; ++dd) nrm[u][3 * f + dd] = ld<R>(gb + u * EB + (C::O_GEO + 12 + 4 * f + dd) * RB);
         const uint4* lgt = reinterpret_cast<const uint4*>(tab + L.lg);
-        for (int a = q; a < NP; a += TG) {
-          const uint4 e = __ldg(lgt + a);
-          const int lo[4] = {(int)(e.x & 0xFFFF), (int)(e.x >> 16), (int)(e.y & 0xFFFF), (int)(e.y >> 16)};
-          R lm[4];
 #pragma unroll
-          for (int f = 0; f < 4; ++f) lm[f] = lam_s[(e.z >> (8 * f)) & 0xFF];
-          const R i1 = __ldg(invfacN + a), i2 = __ldg(invfac2N + a), f1 = __ldg(facN + a);
+        for (int k = 0; k < KO; ++k) {
+          const int a = q + TG * k;
+          if (a < NP) {
+            const uint4 e = __ldg(lgt + a);
+            const int lo[4] = {(int)(e.x & 0xFFFF), (int)(e.x >> 16), (int)(e.y & 0xFFFF), (int)(e.y >> 16)};
+            R lm[4];
 #pragma unroll
-          for (int u = 0; u < ET; ++u) {
-            const char* eb = gb + u * EB;
-            R sp = R(0), sx = R(0), sy = R(0), sz = R(0);
+            for (int f = 0; f < 4; ++f) lm[f] = lam_s[(e.z >> (8 * f)) & 0xFF];
+            const R i1 = __ldg(invfacN + a), i2 = __ldg(invfac2N + a), f1 = __ldg(facN + a);
 #pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              const R wp = lm[f] * ld<R>(eb + (C::S_L + (2 * f) * NP) * RB + lo[f]);
-              const R wu = lm[f] * ld<R>(eb + (C::S_L + (2 * f + 1) * NP) * RB + lo[f]);
-              sp += wp;
-              sx = fma(nrm[u][3 * f], wu, sx);
-              sy = fma(nrm[u][3 * f + 1], wu, sy);
-              sz = fma(nrm[u][3 * f + 2], wu, sz);
-            }
-            const long long k = k0 + u;
-            R rp = fma(sp, i2, ld<R>(eb + (C::O_R + a) * RB));
-            if (A.src && k < A.elem_end) rp = fma(A.src_amp * A.src[k * NP + a], i1, rp);
-            st<R>(gb + u * EB + (C::O_R + a) * RB, rp);
-            const R ru[3] = {fma(ld<R>(eb + (C::O_R + NP + a) * RB), f1, sx * i1),
-                             fma(ld<R>(eb + (C::O_R + 2 * NP + a) * RB), f1, sy * i1),
-                             fma(ld<R>(eb + (C::O_R + 3 * NP + a) * RB), f1, sz * i1)};
-            if (k < A.elem_end) {
+            for (int u = 0; u < ET; ++u) {
+              const char* eb = gb + u * EB;
+              R sp = R(0), sx = R(0), sy = R(0), sz = R(0);
 #pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                const long long gi = k * 4 * NP + (1 + d) * NP + a;
-                if (A.mode == 0) {
-                  const R rs = fma(A.rk_a, ld<R>(eb + (C::O_RS + (1 + d) * NP + a) * RB), A.dt * ru[d]);
-                  A.res[gi] = rs;
-                  A.Qout[gi] = fma(A.rk_b, rs, ld<R>(eb + (C::O_Q + (1 + d) * NP + a) * RB));
-                } else {
-                  A.Qout[gi] = ru[d];
+              for (int f = 0; f < 4; ++f) {
+                const R wp = lm[f] * ld<R>(eb + (C::X_L + (2 * f) * NP) * RB + lo[f]);
+                const R wu = lm[f] * ld<R>(eb + (C::X_L + (2 * f + 1) * NP) * RB + lo[f]);
+                sp += wp;
+                sx = fma(nrm[u][3 * f], wu, sx);
+                sy = fma(nrm[u][3 * f + 1], wu, sy);
+                sz = fma(nrm[u][3 * f + 2], wu, sz);
+              }
+              const long long kk = k0 + u;
+              R rp = fma(sp, i2, ld<R>(eb + (C::O_RP + a) * RB));
+              if (A.src && u < nE) rp = fma(A.src_amp * __ldg(A.src + kk * NP + a), i1, rp);
+              st<R>(gb + u * EB + (C::O_RP + a) * RB, rp);
+              const R r3[3] = {fma(ru[u][0][k], f1, sx * i1), fma(ru[u][1][k], f1, sy * i1),
+                               fma(ru[u][2][k], f1, sz * i1)};
+              if (u < nE) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                  const long long gi = kk * 4 * NP + (1 + d) * NP + a;
+                  if (A.mode == 0) {
+                    const R r = fma(A.rk_a, rs[u][1 + d][k], A.dt * r3[d]);
+                    A.res[gi] = r;
+                    A.Qout[gi] = fma(A.rk_b, r, qo[u][1 + d][k]);
+                  } else {
+                    A.Qout[gi] = r3[d];
+                  }
                 }
               }
             }
           }
         }
       }
-      __syncthreads();
+      sync();
     }
 
     // ---- F-I: WADG multiply + telescoping projection of r_p
-    wadg_phases<C, R>(gb, q, A);
+    wadg_phases<C, R>(gb, q, A, sync);
     constexpr int RES = wadg_result<C>();
 
     // ---- J: dp/dt = a!/N! b_N; outputs
-    for (int a = q; a < NP; a += TG) {
-      const R sc = __ldg(outN + a);
 #pragma unroll
-      for (int u = 0; u < ET; ++u) {
-        const long long k = k0 + u;
-        if (k >= A.elem_end) continue;
-        const R dp = ld<R>(gb + u * EB + (RES + a) * RB) * sc;
-        if (A.mode == 2) {
-          A.Qout[k * NP + a] = dp;
-        } else {
-          const long long gi = k * 4 * NP + a;
-          if (A.mode == 0) {
-            const R rs = fma(A.rk_a, ld<R>(gb + u * EB + (C::O_RS + a) * RB), A.dt * dp);
-            A.res[gi] = rs;
-            A.Qout[gi] = fma(A.rk_b, rs, ld<R>(gb + u * EB + (C::O_Q + a) * RB));
+    for (int k = 0; k < KO; ++k) {
+      const int a = q + TG * k;
+      if (a < NP) {
+        const R sc = __ldg(outN + a);
+#pragma unroll
+        for (int u = 0; u < ET; ++u) {
+          if (u >= nE) continue;
+          const long long kk = k0 + u;
+          const R dp = ld<R>(gb + u * EB + (RES + a) * RB) * sc;
+          if (A.mode == 2) {
+            A.Qout[kk * NP + a] = dp;
           } else {
-            A.Qout[gi] = dp;
+            const long long gi = kk * 4 * NP + a;
+            if (A.mode == 0) {
+              const R r = fma(A.rk_a, rs[u][0][k], A.dt * dp);
+              A.res[gi] = r;
+              A.Qout[gi] = fma(A.rk_b, r, qo[u][0][k]);
+            } else {
+              A.Qout[gi] = dp;
+            }
           }
         }
       }
     }
-    __syncthreads();
+    sync();
   }
 }
 

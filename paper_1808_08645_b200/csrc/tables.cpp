@@ -193,6 +193,13 @@ HostTables build_tables(int N, int M, int RB) {
     W.put<int32_t>(L.csr_ptr, (int)iH.size(), t);
     if (t != lnp3(N) * lnp3(M)) throw std::runtime_error("CSR term count mismatch");
   }
+  // ROWDEC: rows of degree N+M in canonical order
+  {
+    int r = 0;
+    for (int g3 = 0; g3 <= N + M; ++g3)
+      for (int g2 = 0; g2 <= N + M - g3; ++g2)
+        W.put<uint32_t>(L.rowdec, r++, (uint32_t)g2 | ((uint32_t)g3 << 8) | ((uint32_t)rank3(N + M, 0, g2, g3) << 16));
+  }
   // scale arrays
   {
     auto iN = indices3(N), iM = indices3(M), iH = indices3(N + M), iN1 = indices3(N - 1);
