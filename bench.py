@@ -311,7 +311,7 @@ def run_ours(args):
     s.close()
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(N, M, args.cpu_seconds)
-    if rank == 0 and args.sweep:
+    if rank == 0 and not args.no_sweep:
         out["sweep"] = sweep(args, dev)
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -337,7 +337,7 @@ def sweep(args, dev):
         M = N
         Np = comb(N + 3, 3)
         c2 = media.project_c2(v, e, f, M, device=dev)
-        s = Solver(v, e, N, M, c2, device=dev.index, stream=torch.cuda.current_stream(dev), check_c2=False)
+        s = Solver(v, e, N, M, c2, device=dev.index, stream=torch.cuda.current_stream(dev))
         Q0 = torch.randn((len(e), 4, Np), dtype=torch.float64, device=dev)
         s.set_state(Q0)
         del Q0
@@ -424,7 +424,7 @@ def main():
     ap.add_argument("--M", type=int, default=None)
     ap.add_argument("--n-cubes", type=int, default=None)
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
-    ap.add_argument("--sweep", action="store_true", help="append the config-3 N=1..9 sweep")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-3 N=1..9 sweep (rank 0, after the timed run)")
     ap.add_argument("--sweep-n", type=int, default=44)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-random", action="store_true")

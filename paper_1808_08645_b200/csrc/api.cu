@@ -335,7 +335,10 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
     const double* ci = c2 + (size_t)P.gid[i] * c->Mp;
     std::memcpy(&c2l[(size_t)i * c->Mp], ci, sizeof(double) * c->Mp);
     if (o.check_c2) {
-      double mn = chk.min_value(ci);
+      // convex hull property: all Bernstein coefficients > 0 => c^2_M > 0 on the element
+      bool allpos = true;
+      for (int b = 0; b < c->Mp; ++b) allpos = allpos && (ci[b] > 0);
+      double mn = allpos ? 1.0 : chk.min_value(ci);
       if (!(mn > 0)) {
 #pragma omp critical
         {

@@ -268,3 +268,57 @@ def test_group_partition_bitwise(gpu_lib, nparts):
     for c in ctxs:
         L.bbwadg_destroy(c)
     assert np.array_equal(out, ref)
+
+
+# ------------------------------------------------------------------------------------ full sizes
+def _neighbour_closure(e, sample):
+    """sample elements plus every element sharing a face with one of them (numpy face matching)."""
+    K = e.shape[0]
+    faces = np.concatenate([np.sort(e[:, [1, 2, 3]], 1), np.sort(e[:, [0, 2, 3]], 1),
+                            np.sort(e[:, [0, 1, 3]], 1), np.sort(e[:, [0, 1, 2]], 1)])
+    owner = np.concatenate([np.arange(K)] * 4)
+    order = np.lexsort((faces[:, 2], faces[:, 1], faces[:, 0]))
+    sf, so = faces[order], owner[order]
+    same = np.all(sf[1:] == sf[:-1], axis=1)
+    a, b = so[:-1][same], so[1:][same]
+    want = np.zeros(K, dtype=bool)
+    want[sample] = True
+    nb = np.concatenate([b[want[a]], a[want[b]]])
+    return np.unique(np.concatenate([sample, nb]))
+
+
+@pytest.mark.parametrize("cfg", ["config5", "config3_N9", "config4_f32"])
+def test_full_size_sampled_parity(gpu_lib, cfg):
+    """BASELINE.json configs at full size in the bench launch configuration: bbwadg_rhs on the
+    whole mesh; the oracle recomputes 48 sampled elements (with their face neighbours)."""
+    import torch
+
+    if cfg == "config5":
+        n, N, M, f, dtype, tol = 88, 7, 4, media.c2_smooth(1.0), "f64", 1e-12
+    elif cfg == "config3_N9":
+        n, N, M, f, dtype, tol = 44, 9, 9, media.c2_smooth(8.0), "f64", 1e-12
+    else:
+        n, N, M, f, dtype, tol = 56, 5, 3, media.c2_layered(), "f32", 1e-5
+    v, e = kuhn.kuhn_mesh(n)
+    dev = torch.device("cuda", 0)
+    c2 = media.project_c2(v, e, f, M, device=dev)
+    s = _solver(v, e, N, M, c2, dtype=dtype)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1808)
+    Np = states.num_coeffs(N)
+    Q = torch.randn((len(e), 4, Np), dtype=torch.float64, device=dev, generator=gen)
+    if dtype == "f32":
+        Q = Q.float()
+    out = s.rhs(Q, 0.0)
+    rng = np.random.default_rng(5)
+    sample = np.unique(np.concatenate([rng.choice(len(e), 46, replace=False), [0, len(e) - 1]]))
+    sub = _neighbour_closure(e, sample)
+    idx = torch.from_numpy(sub).to(dev)
+    Qs = Q.index_select(0, idx).double().cpu().numpy()
+    got = out.index_select(0, idx).double().cpu().numpy()
+    del out, Q
+    s.close()
+    o = AcousticOracle(v, e[sub], N, M, c2[sub])
+    ref = o.rhs(Qs)
+    pos = np.searchsorted(sub, sample)
+    assert rel_l2(got[pos], ref[pos]) <= tol
