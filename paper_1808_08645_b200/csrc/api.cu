@@ -75,6 +75,7 @@ struct bbwadg_ctx_s {
   void* d_send = nullptr;
   int* d_sendfaces = nullptr;
   int* d_flag = nullptr;
+  unsigned long long* d_ptime = nullptr;  // phase timing counters (BBW_PHASE_TIMING builds)
   // multi-GPU
   nccl::Comm comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -148,6 +149,7 @@ bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, i
     a.dt = dt;
     a.src_amp = std::sin(M_PI * tstage);
     a.mode = mode;
+    a.ptime = c->d_ptime;
     err = c->ks.launch_stage(&a, grid, c->stream);
   } else {
     StageArgs<float> a;
@@ -162,6 +164,7 @@ bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, i
     a.dt = (float)dt;
     a.src_amp = (float)std::sin(M_PI * tstage);
     a.mode = mode;
+    a.ptime = c->d_ptime;
     err = c->ks.launch_stage(&a, grid, c->stream);
   }
   if (err != cudaSuccess) return fail(c, BBWADG_ERR_CUDA, std::string("stage kernel launch: ") + cudaGetErrorString(err));
@@ -370,6 +373,10 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   CUDA_TRY(c.get(), cudaMalloc(&c->d_res, std::max<size_t>(sb, 16)));
   CUDA_TRY(c.get(), cudaMemset(c->d_res, 0, sb));
   CUDA_TRY(c.get(), cudaMalloc(&c->d_flag, sizeof(int)));
+  if (getenv("BBWADG_PHASE_TIMING")) {
+    CUDA_TRY(c.get(), cudaMalloc(&c->d_ptime, 32 * sizeof(unsigned long long)));
+    CUDA_TRY(c.get(), cudaMemset(c->d_ptime, 0, 32 * sizeof(unsigned long long)));
+  }
   const int64_t nghost = P.num_ghost(), nsend = P.send_off.empty() ? 0 : P.send_off.back();
   const size_t per_face = 4 * (size_t)c->Nfp * c->rb;
   if (nghost > 0) CUDA_TRY(c.get(), cudaMalloc(&c->d_ghost, nghost * per_face));
@@ -669,7 +676,7 @@ void bbwadg_destroy(bbwadg_ctx c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* bufs[] = {c->d_tab, c->d_Q[0], c->d_Q[1], c->d_res, c->d_c2, c->d_geo, c->d_nbr, c->d_code,
-                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag};
+                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag, c->d_ptime};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm) nccl::comm_destroy(c->comm);
@@ -777,6 +784,16 @@ int64_t bbwadg_debug_tables(int N, int M, int fp_bytes, void* out, int64_t cap, 
     for (int j = 0; j <= N; ++j) lam[j] = T.lam[j];
   if (out) std::memcpy(out, T.blob.data(), std::min<size_t>(T.blob.size(), (size_t)cap));
   return (int64_t)T.blob.size();
+}
+
+// Debug hook (not in the public header): per-phase cycle counters accumulated by a
+// BBW_PHASE_TIMING build when BBWADG_PHASE_TIMING is set; copies 32 values, resets them.
+int bbwadg_debug_phase_times(bbwadg_ctx c, unsigned long long* out) {
+  if (!c || !c->d_ptime || !out) return -1;
+  cudaStreamSynchronize(c->stream);
+  cudaMemcpy(out, c->d_ptime, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemset(c->d_ptime, 0, 32 * sizeof(unsigned long long));
+  return 0;
 }
 
 const char* bbwadg_version(void) { return "bbwadg-b200 0.1 (sm_100a, fused stage kernel v1)"; }

@@ -57,6 +57,7 @@ struct StageArgs {
   R rk_a, rk_b, dt, src_amp, tau_p, tau_u;
   R gam[10], lam[10];
   int mode;  // 0 LSRK stage, 1 write dQ/dt into Qout, 2 WADG apply (Qin=r[K][NP] -> Qout[K][NP])
+  unsigned long long* ptime;  // BBW_PHASE_TIMING builds only: per-phase cycle counters [32]
 };
 
 #ifndef BBW_T
@@ -91,13 +92,19 @@ struct StageCfg {
   static constexpr int G = T / TG;               // groups per CTA
   static constexpr int KO = (NP + TG - 1) / TG;  // owned coefficients per thread
   // ---- per-element shared-memory layout (in reals)
-  static constexpr int O_GEO = 0, O_C = 32, O_RP = 32 + MP;
+  static constexpr int O_GEO = 0, O_C = 40, O_RP = 40 + MP;  // GEO: grad l (12), normals+|grad l| (16), nbr/code ints
   static constexpr int O_X = rup(O_RP + NP, VEC);
   static constexpr int X_Q = O_X, X_G = O_X + 4 * NP, X_L = O_X;  // Q + G'', later the lift layers
   static constexpr int XSIZE = cmax(4 * NP + 4 * (NPM1 + 1), 8 * NP);
   static constexpr int O_Y = O_X + XSIZE;
   static constexpr int Y_F = O_Y, Y_Y = O_Y + 8 * NFP;  // F', Y''
-  static constexpr int YSIZE = 8 * NFP + 8 * (NFP1 + 1);
+  static constexpr int YSIZE = cmax(8 * NFP + 8 * (NFP1 + 1), NFP * (N + 1));
+  static constexpr int Y_RPP = O_Y;  // zero-padded rows of r''_p (stride N+1), written in E, read by F
+#ifdef BBW_PAD_MIN_M
+  static constexpr bool PAD = (M >= BBW_PAD_MIN_M);
+#else
+  static constexpr bool PAD = (M >= 6);  // padded row copy pays off only for long product rows
+#endif
   static constexpr int W_H = O_X, W_P = W_H + NPH, W_LEV = W_P + NPH;  // WADG (aliases X, Y)
   static constexpr int W_A0 = W_LEV + NP4, W_A1 = W_A0 + NP + 1;
   static constexpr int WSIZE = 2 * NPH + NP4 + 2 * (NP + 1);
@@ -119,6 +126,21 @@ struct GroupSync {
     }
   }
 };
+
+#ifdef BBW_PHASE_TIMING
+#define BBW_PT(id)                                                     \
+  do {                                                                 \
+    if (q == 0 && A.ptime) {                                           \
+      const long long t_ = clock64();                                  \
+      atomicAdd(A.ptime + (id), (unsigned long long)(t_ - pt_prev));   \
+      pt_prev = t_;                                                    \
+    }                                                                  \
+  } while (0)
+#else
+#define BBW_PT(id) \
+  do {             \
+  } while (0)
+#endif
 
 template <typename R>
 __device__ __forceinline__ R ld(const char* p) { return *reinterpret_cast<const R*>(p); }
@@ -192,7 +214,8 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
 }
 
 template <class C, typename R>
-__device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync) {
+__device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync,
+                                            long long& pt_prev) {
   constexpr int N = C::N, M = C::M, NP = C::NP, NPH = C::NPH, RB = C::RB, ET = C::ET, EB = C::EB, TG = C::TG;
   constexpr TabLayout L = tab_layout(N, M, RB);
   const uint8_t* tab = A.tab;
@@ -226,14 +249,22 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
             constexpr int CB = cnp3(M) - cnp3(M - b3) + b2 * (2 * (M - b3) + 3 - b2) / 2;  // rank_M(0,b2,b3)
             const int a2 = g2 - b2, a3 = g3 - b3;
             if (a2 >= 0 && a3 >= 0 && a2 + a3 <= N) {
-              const int m = N - a3, la = m - a2 + 1;
-              const int ra = (cnp3(N) - (m + 1) * (m + 2) * (m + 3) / 6 + a2 * (2 * m + 3 - a2) / 2) * RB;
-              const char* pr = gb + C::O_RP * RB + ra;
+              const char* pr;
+              int la = N + 1;
+              if constexpr (C::PAD) {
+                const int rowid = a3 * (2 * N + 3 - a3) / 2 + a2;
+                pr = gb + C::Y_RPP * RB + rowid * ((N + 1) * RB);
+              } else {
+                const int m = N - a3;
+                la = m - a2 + 1;
+                pr = gb + C::O_RP * RB + (cnp3(N) - (m + 1) * (m + 2) * (m + 3) / 6 + a2 * (2 * m + 3 - a2) / 2) * RB;
+              }
 #pragma unroll
               for (int u = 0; u < ET; ++u) {
                 R in[N + 1];
 #pragma unroll
-                for (int a1 = 0; a1 <= N; ++a1) in[a1] = (a1 < la) ? ld<R>(pr + a1 * RB + u * EB) : R(0);
+                for (int a1 = 0; a1 <= N; ++a1)
+                  in[a1] = (C::PAD || a1 < la) ? ld<R>(pr + a1 * RB + u * EB) : R(0);
 #pragma unroll
                 for (int b1 = 0; b1 < LB; ++b1) {
                   const R cv = ld<R>(gb + (C::O_C + CB + b1) * RB + u * EB);
@@ -264,6 +295,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
     }
   }
   sync();
+  BBW_PT(6);
   // G: M reductions N+M -> N (ping-pong H <-> P; the last lands in level N)
   static_for<N + M, N, -1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
@@ -272,6 +304,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
     constexpr int DST = (n - 1 == N) ? C::W_LEV + cnp4(N - 1) : ((k % 2 == 0) ? C::W_P : C::W_H);
     sum4_phase<C, R, cnp3(n - 1), SRC, DST>(gb, q, red + red_off(n));
     sync();
+    BBW_PT(7);
   });
   if constexpr (M == 0) {
     for (int i = q; i < NP; i += TG)
@@ -279,12 +312,14 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
       for (int u = 0; u < ET; ++u)
         st<R>(gb + (C::W_LEV + cnp4(N - 1) + i) * RB + u * EB, ld<R>(gb + (C::W_H + i) * RB + u * EB));
     sync();
+    BBW_PT(7);
   }
   // H: downward reductions level n -> n-1
   static_for<N, 0, -1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
     sum4_phase<C, R, cnp3(n - 1), C::W_LEV + cnp4(n - 1), C::W_LEV + cnp4(n - 2)>(gb, q, red + red_off(n));
     sync();
+    BBW_PT(8);
   });
   // I: upward: b_n[a] = sum_j b_{n-1}[a - e_j] + gam_n/(a!)^2 u_n[a]   (b_n in A_{n%2}, b_0 = gam_0 u_0)
   static_for<1, N + 1, 1>([&](auto nc) {
@@ -332,6 +367,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
       }
     }
     sync();
+    BBW_PT(9);
   });
 }
 
@@ -369,6 +405,8 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
   const long long nbatch = (nelem + ET - 1) / ET;
   for (long long batch = (long long)blockIdx.x * C::G + grp; batch < nbatch; batch += (long long)gridDim.x * C::G) {
     const long long k0 = A.elem_begin + batch * ET;
+    long long pt_prev = clock64();
+    (void)pt_prev;
     const int nE = (int)((A.elem_end - k0) < ET ? (A.elem_end - k0) : ET);
 
     // ---- A: loads (residual -> registers; Q -> smem; geometry, c'' -> smem; zero slots)
@@ -385,9 +423,20 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
           }
     }
     if (A.mode == 2) {
+      const uint16_t* padoff = reinterpret_cast<const uint16_t*>(tab + L.padoff);
       for (int t = q; t < nE * NP; t += TG) {
         const int u = t / NP, a = t - u * NP;
-        st<R>(gb + u * EB + (C::O_RP + a) * RB, A.Qin[(k0 + u) * NP + a] * __ldg(invfacN + a));
+        const R v = A.Qin[(k0 + u) * NP + a] * __ldg(invfacN + a);
+        st<R>(gb + u * EB + (C::O_RP + a) * RB, v);
+        st<R>(gb + u * EB + C::Y_RPP * RB + __ldg(padoff + a), v);
+      }
+      constexpr int NS = NFP * (N + 1);
+      for (int t = q; t < NS; t += TG) {
+        const int row = t / (N + 1), a1 = t - row * (N + 1);
+        if (a1 >= (int)__ldg(tab + L.rowlen + row)) {
+#pragma unroll
+          for (int u = 0; u < ET; ++u) st<R>(gb + u * EB + (C::Y_RPP + t) * RB, R(0));
+        }
       }
     } else {
       constexpr int NV = 4 * NP / VEC;
@@ -396,6 +445,12 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
       for (int t = q; t < nE * NV; t += TG) {
         const int u = t / NV, w = t - u * NV;
         *reinterpret_cast<V*>(gb + u * EB + C::X_Q * RB + w * 16) = __ldg(gq + t);
+      }
+      for (int t = q; t < nE * 4; t += TG) {  // neighbour id and code of every face
+        const int u = t >> 2, f = t & 3;
+        int* nbs = reinterpret_cast<int*>(gb + u * EB + 28 * RB);
+        nbs[f] = __ldg(A.nbr + (k0 + u) * 4 + f);
+        nbs[4 + f] = __ldg(A.code + (k0 + u) * 4 + f);
       }
       for (int t = q; t < nE * 4; t += TG) {  // grad lambda_f, outward normal, |grad lambda_f|
         const int u = t >> 2, f = t & 3;
@@ -422,6 +477,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
       st<R>(gb + u * EB + (C::O_C + b) * RB, __ldg(A.c2 + (k0 + u) * MP + b) * __ldg(invfacM + b));
     }
     sync();
+    BBW_PT(0);
 
     R qo[ET][4][KO];  // own Q_in coefficients (LSRK)
     R ru[ET][3][KO];  // own r_u (x/a! scaled until phase E)
@@ -436,42 +492,52 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
             const int a = q + TG * k;
             qo[u][c][k] = (a < NP) ? ld<R>(gb + u * EB + (C::X_Q + c * NP + a) * RB) : R(0);
           }
-      // ---- B1: fluxes, F' = |grad l_f| c! F
-      for (int t = q; t < 4 * NFP; t += TG) {
-        const int f = t / NFP, i = t - f * NFP;
-        const int own = __ldg(fnode + f * NFP + i);
-        const R cs = __ldg(cfac + i);
+      // ---- B1: fluxes, F' = |grad l_f| c! F.  All items of the thread are unrolled so the neighbour
+      //      trace loads (L2) of every item are in flight together.
+      {
+        constexpr int NI = 4 * NFP, K1 = (NI + TG - 1) / TG;
 #pragma unroll
-        for (int u = 0; u < ET; ++u) {
-          const char* eb = gb + u * EB + C::X_Q * RB;
-          const long long k = k0 + u;
-          const R pm = ld<R>(eb + own), uxm = ld<R>(eb + own + NP * RB), uym = ld<R>(eb + own + 2 * NP * RB),
-                  uzm = ld<R>(eb + own + 3 * NP * RB);
-          R pp = -pm, uxp = uxm, uyp = uym, uzp = uzm;
-          if (u < nE) {
-            const int nb = __ldg(A.nbr + k * 4 + f);
-            if (nb >= 0) {
-              const int vol = __ldg(nbrvol + __ldg(A.code + k * 4 + f) * NFP + i);
-              const R* qn = A.Qin + (long long)nb * 4 * NP + vol;
-              pp = __ldg(qn);
-              uxp = __ldg(qn + NP);
-              uyp = __ldg(qn + 2 * NP);
-              uzp = __ldg(qn + 3 * NP);
-            } else if (nb < -1) {
-              const int fi = __ldg(nbrface + (__ldg(A.code + k * 4 + f) % 6) * NFP + i);
-              const R* gh = A.ghost + (long long)(-2 - nb) * 4 * NFP + fi;
-              pp = gh[0];
-              uxp = gh[NFP];
-              uyp = gh[2 * NFP];
-              uzp = gh[3 * NFP];
+        for (int k = 0; k < K1; ++k) {
+          const int t = q + TG * k;
+          const bool act = (NI % TG == 0) || t < NI;
+          const int tc = act ? t : 0;
+          const int f = tc / NFP, i = tc - f * NFP;
+          const int own = __ldg(fnode + f * NFP + i);
+          const R cs = __ldg(cfac + i);
+#pragma unroll
+          for (int u = 0; u < ET; ++u) {
+            const char* eb = gb + u * EB + C::X_Q * RB;
+            const int* nbs = reinterpret_cast<const int*>(gb + u * EB + 28 * RB);
+            const int nb = nbs[f], code = nbs[4 + f];
+            const R pm = ld<R>(eb + own), uxm = ld<R>(eb + own + NP * RB), uym = ld<R>(eb + own + 2 * NP * RB),
+                    uzm = ld<R>(eb + own + 3 * NP * RB);
+            R pp = -pm, uxp = uxm, uyp = uym, uzp = uzm;
+            if (act && u < nE) {
+              if (nb >= 0) {
+                const int vol = __ldg(nbrvol + code * NFP + i);
+                const R* qn = A.Qin + (long long)nb * 4 * NP + vol;
+                pp = __ldg(qn);
+                uxp = __ldg(qn + NP);
+                uyp = __ldg(qn + 2 * NP);
+                uzp = __ldg(qn + 3 * NP);
+              } else if (nb < -1) {
+                const int fi = __ldg(nbrface + (code % 6) * NFP + i);
+                const R* gh = A.ghost + (long long)(-2 - nb) * 4 * NFP + fi;
+                pp = gh[0];
+                uxp = gh[NFP];
+                uyp = gh[2 * NFP];
+                uzp = gh[3 * NFP];
+              }
+            }
+            const char* gs = gb + u * EB + (C::O_GEO + 12 + 4 * f) * RB;
+            const R nx = ld<R>(gs), ny = ld<R>(gs + RB), nz = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * cs;
+            const R jp = pp - pm;
+            const R jun = nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
+            if (act) {
+              st<R>(gb + u * EB + (C::Y_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));
+              st<R>(gb + u * EB + (C::Y_F + (2 * f + 1) * NFP + i) * RB, R(0.5) * sc * (A.tau_u * jun - jp));
             }
           }
-          const char* gs = gb + u * EB + (C::O_GEO + 12 + 4 * f) * RB;
-          const R nx = ld<R>(gs), ny = ld<R>(gs + RB), nz = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * cs;
-          const R jp = pp - pm;
-          const R jun = nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
-          st<R>(gb + u * EB + (C::Y_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));
-          st<R>(gb + u * EB + (C::Y_F + (2 * f + 1) * NFP + i) * RB, R(0.5) * sc * (A.tau_u * jun - jp));
         }
       }
       // ---- B2: g''_b = sum_i grad(l_i) q_{b+e_i} / b!   (div u, grad p)
@@ -510,6 +576,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
         }
       }
       sync();
+      BBW_PT(1);
       // ---- C1: r''_c[a] = -sum_j g''_c[a - e_j]  (p -> smem R_p, u -> registers)
       {
         const ushort4* ve = reinterpret_cast<const ushort4*>(tab + L.ve);
@@ -544,6 +611,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
           gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(N - 1),
           reinterpret_cast<const R*>(tab + L.s_invf2));
       sync();
+      BBW_PT(2);
       // ---- C3: layer 0: w'_0[c] = (2N+3) F'[c] + (c!)^2 sum_s Y''[c - e_s]
       {
         const ushort4* te = reinterpret_cast<const ushort4*>(tab + L.triele);
@@ -563,6 +631,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
         }
       }
       sync();
+      BBW_PT(3);
       // ---- D: lift layers j = 1..N: w'_j[d] = sum_s w'_{j-1}[d + e_s]
       static_for<1, N + 1, 1>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
@@ -570,9 +639,23 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
         face_sum3<C, R, cnp2(m), C::X_L + layer_off(N, j - 1), NP, C::X_L + layer_off(N, j), NP, false>(
             gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(m), static_cast<const R*>(nullptr));
         sync();
+        BBW_PT(4);
       });
       // ---- E: gather lifts; r''_p += S_p/(a!)^2 (+ source) -> smem; r_u = a! r''_u + S_u/a!; LSRK for u
+      //      r''_p also goes to a zero-padded row copy (row stride N+1) in the dead face region for F
+      if constexpr (C::PAD) {
+        constexpr int NS = NFP * (N + 1);
+        const uint8_t* rowlen = tab + L.rowlen;
+        for (int t = q; t < NS; t += TG) {
+          const int row = t / (N + 1), a1 = t - row * (N + 1);
+          if (a1 >= (int)__ldg(rowlen + row)) {
+#pragma unroll
+            for (int u = 0; u < ET; ++u) st<R>(gb + u * EB + (C::Y_RPP + t) * RB, R(0));
+          }
+        }
+      }
       {
+        const uint16_t* padoff = reinterpret_cast<const uint16_t*>(tab + L.padoff);
         R nrm[ET][12];  // outward normals of the group's elements, hoisted into registers
 #pragma unroll
         for (int u = 0; u < ET; ++u)
@@ -591,6 +674,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
 #pragma unroll
             for (int f = 0; f < 4; ++f) lm[f] = lam_s[(e.z >> (8 * f)) & 0xFF];
             const R i1 = __ldg(invfacN + a), i2 = __ldg(invfac2N + a), f1 = __ldg(facN + a);
+            const int pado = __ldg(padoff + a);
 #pragma unroll
             for (int u = 0; u < ET; ++u) {
               const char* eb = gb + u * EB;
@@ -608,6 +692,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
               R rp = fma(sp, i2, ld<R>(eb + (C::O_RP + a) * RB));
               if (A.src && u < nE) rp = fma(A.src_amp * __ldg(A.src + kk * NP + a), i1, rp);
               st<R>(gb + u * EB + (C::O_RP + a) * RB, rp);
+              if constexpr (C::PAD) st<R>(gb + u * EB + C::Y_RPP * RB + pado, rp);
               const R r3[3] = {fma(ru[u][0][k], f1, sx * i1), fma(ru[u][1][k], f1, sy * i1),
                                fma(ru[u][2][k], f1, sz * i1)};
               if (u < nE) {
@@ -628,10 +713,11 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
         }
       }
       sync();
+      BBW_PT(5);
     }
 
     // ---- F-I: WADG multiply + telescoping projection of r_p
-    wadg_phases<C, R>(gb, q, A, sync);
+    wadg_phases<C, R>(gb, q, A, sync, pt_prev);
     constexpr int RES = wadg_result<C>();
 
     // ---- J: dp/dt = a!/N! b_N; outputs
@@ -661,6 +747,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
       }
     }
     sync();
+    BBW_PT(10);
   }
 }
 

@@ -200,6 +200,18 @@ HostTables build_tables(int N, int M, int RB) {
       for (int g2 = 0; g2 <= N + M - g3; ++g2)
         W.put<uint32_t>(L.rowdec, r++, (uint32_t)g2 | ((uint32_t)g3 << 8) | ((uint32_t)rank3(N + M, 0, g2, g3) << 16));
   }
+  // PADOFF / ROWLEN: zero-padded row copy of degree-N arrays (row (a2,a3) at rowid*(N+1))
+  {
+    auto idx = indices3(N);
+    for (size_t i = 0; i < idx.size(); ++i) {
+      const int* a = idx[i].a;
+      const int rowid = a[3] * (2 * N + 3 - a[3]) / 2 + a[2];
+      W.put<uint16_t>(L.padoff, (int)i, (uint16_t)((rowid * (N + 1) + a[1]) * RB));
+    }
+    int r = 0;
+    for (int a3 = 0; a3 <= N; ++a3)
+      for (int a2 = 0; a2 <= N - a3; ++a2) W.put<uint8_t>(L.rowlen, r++, (uint8_t)(N - a2 - a3 + 1));
+  }
   // scale arrays
   {
     auto iN = indices3(N), iM = indices3(M), iH = indices3(N + M), iN1 = indices3(N - 1);
