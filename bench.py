@@ -178,6 +178,7 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # (oversubscription only for debugging)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
