@@ -312,6 +312,10 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   int nsm = 0;
   CUDA_TRY(c.get(), cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
   c->grid = nsm * c->ks.blocks_per_sm();
+  if (const char* e = getenv("BBWADG_BLOCKS_PER_SM")) {  // tuning: occupancy sensitivity experiments
+    const int b = atoi(e);
+    if (b > 0 && b < c->ks.blocks_per_sm()) c->grid = nsm * b;
+  }
   // NULL selects the legacy default stream (stream 0), so that work is ordered with
   // torch's default stream and every other legacy-stream user (cuBLAS convention).
   c->stream = shared_stream ? shared_stream : static_cast<cudaStream_t>(o.cuda_stream);

@@ -62,7 +62,23 @@ struct MLoop<N, -1> {
 
 }  // namespace bbw
 
+#ifdef BBW_ONLY_NM  // tuning builds: instantiate a single (N, M) = (BBW_ONLY_NM / 10, BBW_ONLY_NM % 10)
+namespace bbw {
+template <int n>
+KernelSet only_nm(int M, int dtype) {
+  if constexpr (n == BBW_ONLY_NM / 10) {
+    if (M == BBW_ONLY_NM % 10) return pick<n, BBW_ONLY_NM % 10>(dtype);
+  }
+  return KernelSet();
+}
+}  // namespace bbw
+#define BBW_INSTANTIATE(n) \
+  namespace bbw {          \
+  KernelSet get_kernels_N##n(int M, int dtype) { return only_nm<n>(M, dtype); } \
+  }
+#else
 #define BBW_INSTANTIATE(n)                                                            \
   namespace bbw {                                                                     \
   KernelSet get_kernels_N##n(int M, int dtype) { return MLoop<n, n>::get(M, dtype); } \
   }
+#endif

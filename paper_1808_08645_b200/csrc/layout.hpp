@@ -38,7 +38,7 @@ struct TabLayout {
 // NBRFACE [6][Np2(N)]       uint16: neighbour face-local index (ghost traces)
 // CSR   ptr [Np(N+M)+1] int32, terms [Np(N) Np(M)] uint32 (alpha*RB | beta*RB << 16)
 // ROWDEC [Np2(N+M)]        uint32: rows (g2, g3) of degree N+M: g2 | g3 << 8 | rank_{N+M}(0,g2,g3) << 16
-// PADOFF [Np(N)]           uint16: byte offset of a in the zero-padded row copy (row stride N+1)
+// PADOFF [Np(N)]           uint16: byte offset of a in the zero-padded row copy (row stride RS)
 // ROWLEN [Np2(N)]          uint8: length N - a2 - a3 + 1 of row (a2, a3) of degree N
 // scale arrays (reals): 1/a!, a!, 1/(a!)^2, a!/N! (deg N); 1/b! (deg M); (g!)^2 N! M!/(N+M)! (deg N+M);
 //                       1/b! (deg N-1); c!, 1/(d!)^2 (deg N-1), (c!)^2 (face, deg N)

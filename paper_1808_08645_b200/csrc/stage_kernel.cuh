@@ -98,13 +98,12 @@ struct StageCfg {
   static constexpr int XSIZE = cmax(4 * NP + 4 * (NPM1 + 1), 8 * NP);
   static constexpr int O_Y = O_X + XSIZE;
   static constexpr int Y_F = O_Y, Y_Y = O_Y + 8 * NFP;  // F', Y''
-  static constexpr int YSIZE = cmax(8 * NFP + 8 * (NFP1 + 1), NFP * (N + 1));
-  static constexpr int Y_RPP = O_Y;  // zero-padded rows of r''_p (stride N+1), written in E, read by F
-#ifdef BBW_PAD_MIN_M
-  static constexpr bool PAD = (M >= BBW_PAD_MIN_M);
-#else
-  static constexpr bool PAD = (M >= 6);  // padded row copy pays off only for long product rows
-#endif
+  // zero-padded rows of r''_p for the product: row (a2,a3) at rowid * RS (RS = N+1 rounded up to an
+  // odd number of 16-B vectors, against bank conflicts), then one all-zero row; written in E, read by F
+  static constexpr int RS = rup(N + 1, VEC) + ((rup(N + 1, VEC) / VEC) % 2 == 0 ? VEC : 0);  // odd # of vectors
+  static constexpr int NS = (NFP + 1) * RS;
+  static constexpr int YSIZE = cmax(cmax(8 * NFP + 8 * (NFP1 + 1), NS), 0);
+  static constexpr int Y_RPP = O_Y;
   static constexpr int W_H = O_X, W_P = W_H + NPH, W_LEV = W_P + NPH;  // WADG (aliases X, Y)
   static constexpr int W_A0 = W_LEV + NP4, W_A1 = W_A0 + NP + 1;
   static constexpr int WSIZE = 2 * NPH + NP4 + 2 * (NP + 1);
@@ -141,6 +140,64 @@ struct GroupSync {
   do {             \
   } while (0)
 #endif
+
+// switch (n) { case 10: f(9); case 9: f(8); ... case 1: f(0); } with fall-through: runs f(n-1..0)
+#define BBW_FALLTHROUGH_SWITCH(n, f)                   \
+  switch (n) {                                         \
+    case 10: f(std::integral_constant<int, 9>{}); [[fallthrough]]; \
+    case 9: f(std::integral_constant<int, 8>{}); [[fallthrough]];  \
+    case 8: f(std::integral_constant<int, 7>{}); [[fallthrough]];  \
+    case 7: f(std::integral_constant<int, 6>{}); [[fallthrough]];  \
+    case 6: f(std::integral_constant<int, 5>{}); [[fallthrough]];  \
+    case 5: f(std::integral_constant<int, 4>{}); [[fallthrough]];  \
+    case 4: f(std::integral_constant<int, 3>{}); [[fallthrough]];  \
+    case 3: f(std::integral_constant<int, 2>{}); [[fallthrough]];  \
+    case 2: f(std::integral_constant<int, 1>{}); [[fallthrough]];  \
+    case 1: f(std::integral_constant<int, 0>{}); [[fallthrough]];  \
+    default: break;                                    \
+  }
+
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+template <typename R>
+__device__ __forceinline__ void cp_async_real(void* smem, const R* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem),
+               "n"((int)sizeof(R))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+#ifndef BBW_PF
+#define BBW_PF 1
+#endif
+#ifndef BBW_LSRK_REG
+#define BBW_LSRK_REG 1
+#endif
+#ifndef BBW_CPASYNC
+#define BBW_CPASYNC 1
+#endif
+
+// predicated 16-B shared load into x[0..VEC): registers keep their old values when !p
+template <typename R, int OFF>
+__device__ __forceinline__ void ld_shared_vec_pred(R* x, unsigned addr, bool p) {
+  if constexpr (sizeof(R) == 8) {
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.v2.f64 {%0, %1}, [%3+%4];\n}\n"
+        : "+d"(x[0]), "+d"(x[1])
+        : "r"((int)p), "r"(addr), "n"(OFF));
+  } else {
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n @q ld.shared.v4.f32 {%0, %1, %2, %3}, [%5+%6];\n}\n"
+        : "+f"(x[0]), "+f"(x[1]), "+f"(x[2]), "+f"(x[3])
+        : "r"((int)p), "r"(addr), "n"(OFF));
+  }
+}
 
 template <typename R>
 __device__ __forceinline__ R ld(const char* p) { return *reinterpret_cast<const R*>(p); }
@@ -213,6 +270,16 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
   }
 }
 
+// zero reals [off, off + cnt) of every element of the group with 16-B stores (off, cnt multiples of VEC)
+template <class C>
+__device__ __forceinline__ void zero_region(char* gb, int q, int off, int cnt) {
+  const int nv = cnt / C::VEC;
+  for (int t = q; t < C::ET * nv; t += C::TG) {
+    const int u = t / nv, w = t - u * nv;
+    *reinterpret_cast<uint4*>(gb + u * C::EB + off * C::RB + 16 * w) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 template <class C, typename R>
 __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync,
                                             long long& pt_prev) {
@@ -230,6 +297,12 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   {
     constexpr int NR = cnp2(N + M), KR = (NR + TG - 1) / TG;
     const uint32_t* rowdec = reinterpret_cast<const uint32_t*>(tab + L.rowdec);
+    // Rows are stored in order of increasing g2 + g3 (tables.cpp), so the rows of one warp pass
+    // have similar lengths.  r'' is read from its zero-padded row copy (16-B vector loads; lanes
+    // whose input row does not exist read the zero row), and the unrolled a1 steps beyond the
+    // warp's longest input row (la_max = N+1 - (min g2+g3 over the warp) + b2 + b3) are skipped by
+    // warp-uniform branches, so the FMA count follows the real row lengths.
+#if BBW_PROD_V3  // round-1 v3 product (output rows in canonical order, divergent per c-row)
 #pragma unroll 1
     for (int k = 0; k < KR; ++k) {
       const int rho = q + TG * k;
@@ -249,22 +322,15 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
             constexpr int CB = cnp3(M) - cnp3(M - b3) + b2 * (2 * (M - b3) + 3 - b2) / 2;  // rank_M(0,b2,b3)
             const int a2 = g2 - b2, a3 = g3 - b3;
             if (a2 >= 0 && a3 >= 0 && a2 + a3 <= N) {
-              const char* pr;
-              int la = N + 1;
-              if constexpr (C::PAD) {
-                const int rowid = a3 * (2 * N + 3 - a3) / 2 + a2;
-                pr = gb + C::Y_RPP * RB + rowid * ((N + 1) * RB);
-              } else {
-                const int m = N - a3;
-                la = m - a2 + 1;
-                pr = gb + C::O_RP * RB + (cnp3(N) - (m + 1) * (m + 2) * (m + 3) / 6 + a2 * (2 * m + 3 - a2) / 2) * RB;
-              }
+              const int m = N - a3;
+              const int la = m - a2 + 1;
+              const char* pr = gb + C::O_RP * RB + (cnp3(N) - (m + 1) * (m + 2) * (m + 3) / 6 + a2 * (2 * m + 3 - a2) / 2) * RB;
 #pragma unroll
               for (int u = 0; u < ET; ++u) {
                 R in[N + 1];
 #pragma unroll
                 for (int a1 = 0; a1 <= N; ++a1)
-                  in[a1] = (C::PAD || a1 < la) ? ld<R>(pr + a1 * RB + u * EB) : R(0);
+                  in[a1] = (a1 < la) ? ld<R>(pr + a1 * RB + u * EB) : R(0);
 #pragma unroll
                 for (int b1 = 0; b1 < LB; ++b1) {
                   const R cv = ld<R>(gb + (C::O_C + CB + b1) * RB + u * EB);
@@ -286,16 +352,83 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         }
       }
     }
+#else
+    constexpr int VEC = C::VEC, RS = C::RS;
+    R x[RS + VEC];
+#pragma unroll
+    for (int i = 0; i < RS + VEC; ++i) x[i] = R(0);
+#pragma unroll 1
+    for (int k = 0; k < KR; ++k) {
+      const int rho = q + TG * k;
+      const bool act = rho < NR;
+      const uint32_t d = __ldg(rowdec + (act ? rho : NR - 1));
+      const int g2 = d & 0xFF, g3 = (d >> 8) & 0xFF, gs = (int)(d >> 16);
+      const int smin = __reduce_min_sync(0xffffffffu, act ? g2 + g3 : 4 * (N + M));
+      // rowid(a2, a3) = a3 (2N+3-a3)/2 + a2 at a = G - B: rid0 + b3 g3 - b3 (2N+3+b3)/2 - b2
+      const int rid0 = g3 * (2 * N + 3 - g3) / 2 + g2;
+      R acc[ET][N + M + 1];
+#pragma unroll
+      for (int u = 0; u < ET; ++u)
+#pragma unroll
+        for (int x = 0; x <= N + M; ++x) acc[u][x] = R(0);
+      static_for<0, M + 1, 1>([&](auto b3c) {
+        constexpr int b3 = decltype(b3c)::value;
+        const int rid3 = rid0 + b3 * g3 - b3 * (2 * N + 3 + b3) / 2;
+        static_for<0, M + 1 - b3, 1>([&](auto b2c) {
+          constexpr int b2 = decltype(b2c)::value;
+          constexpr int LB = M - b2 - b3 + 1;
+          constexpr int CB = cnp3(M) - cnp3(M - b3) + b2 * (2 * (M - b3) + 3 - b2) / 2;  // rank_M(0,b2,b3)
+          const int a2 = g2 - b2, a3 = g3 - b3;
+          const bool valid = act && a2 >= 0 && a3 >= 0 && a2 + a3 <= N;
+          if (__any_sync(0xffffffffu, valid)) {
+            const int lamax = cmin(N + 1, N + 1 - smin + b2 + b3);
+            const char* pr = gb + (C::Y_RPP + (valid ? rid3 - b2 : C::NFP) * RS) * RB;
+#pragma unroll
+            for (int u = 0; u < ET; ++u) {
+              R cv[LB];
+#pragma unroll
+              for (int b1 = 0; b1 < LB; ++b1) cv[b1] = ld<R>(gb + (C::O_C + CB + b1) * RB + u * EB);
+              // only the vectors below the warp's la_max are loaded (predicated; x keeps stale values
+              // above it, which the FMAs below never read)
+              const unsigned pa = (unsigned)__cvta_generic_to_shared(pr + u * EB);
+              static_for<0, N + 1, VEC>([&](auto a1c) {
+                constexpr int a1 = decltype(a1c)::value;
+                ld_shared_vec_pred<R, a1 * C::RB>(&x[a1], pa, a1 < lamax);
+              });
+              static_for<0, N + 1, 1>([&](auto a1c) {
+                constexpr int a1 = decltype(a1c)::value;
+                if (a1 < lamax) {
+#pragma unroll
+                  for (int b1 = 0; b1 < LB; ++b1) acc[u][a1 + b1] = fma(cv[b1], x[a1], acc[u][a1 + b1]);
+                }
+              });
+            }
+          }
+        });
+      });
+      if (act) {
+        const int lg = N + M - g2 - g3 + 1;
+#pragma unroll
+        for (int x = 0; x <= N + M; ++x) {
+          if (x < lg) {
+            const R s = __ldg(post + gs + x);
+#pragma unroll
+            for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + gs + x) * RB + u * EB, acc[u][x] * s);
+          }
+        }
+      }
+    }
+#endif
   }
-  if (q == 0) {
+  sync();
+  BBW_PT(6);
+  if (q == 0) {  // zero slots of the upward-sweep arrays (may alias the padded rows read above)
 #pragma unroll
     for (int u = 0; u < ET; ++u) {
       st<R>(gb + C::W_A0 * RB + u * EB, R(0));
       st<R>(gb + C::W_A1 * RB + u * EB, R(0));
     }
   }
-  sync();
-  BBW_PT(6);
   // G: M reductions N+M -> N (ping-pong H <-> P; the last lands in level N)
   static_for<N + M, N, -1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
@@ -409,8 +542,10 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
     (void)pt_prev;
     const int nE = (int)((A.elem_end - k0) < ET ? (A.elem_end - k0) : ET);
 
-    // ---- A: loads (residual -> registers; Q -> smem; geometry, c'' -> smem; zero slots)
-    R rs[ET][4][KO];
+    // ---- A: loads (Q, geometry, c'' -> smem via cp.async; the residual is only prefetched into L2
+    //      here and read in phases D and J, so no registers are held across the WADG phases)
+#if BBW_LSRK_REG
+    R rs[ET][4][KO];  // LSRK residual: loaded now, consumed at the end (HBM latency hidden)
     if (A.mode == 0) {
 #pragma unroll
       for (int u = 0; u < ET; ++u)
@@ -419,10 +554,19 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
 #pragma unroll
           for (int k = 0; k < KO; ++k) {
             const int a = q + TG * k;
-            rs[u][c][k] = (u < nE && a < NP) ? __ldg(A.res + (k0 + u) * 4 * NP + c * NP + a) : R(0);
+            rs[u][c][k] = (u < nE && a < NP) ? __ldcs(A.res + (k0 + u) * 4 * NP + c * NP + a) : R(0);
           }
     }
+#else
+    if (A.mode == 0) {
+      const int nl = (nE * 4 * NP * RB + 127) / 128;
+      const char* pr = reinterpret_cast<const char*>(A.res + k0 * 4 * NP);
+      for (int l = q; l < nl; l += TG) prefetch_l2(pr + 128 * l);
+    }
+#endif
     if (A.mode == 2) {
+      zero_region<C>(gb, q, C::Y_RPP, C::NS);
+      sync();
       const uint16_t* padoff = reinterpret_cast<const uint16_t*>(tab + L.padoff);
       for (int t = q; t < nE * NP; t += TG) {
         const int u = t / NP, a = t - u * NP;
@@ -430,15 +574,70 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
         st<R>(gb + u * EB + (C::O_RP + a) * RB, v);
         st<R>(gb + u * EB + C::Y_RPP * RB + __ldg(padoff + a), v);
       }
-      constexpr int NS = NFP * (N + 1);
-      for (int t = q; t < NS; t += TG) {
-        const int row = t / (N + 1), a1 = t - row * (N + 1);
-        if (a1 >= (int)__ldg(tab + L.rowlen + row)) {
+    } else {
+#if BBW_CPASYNC
+      // one round trip: every per-element input goes global -> shared with cp.async (LDGSTS)
+      constexpr int NV = 4 * NP / VEC;  // 16-B chunks of Q
+      constexpr int GV = 12 * RB / 16;  // 16-B chunks of grad(lambda)
+      const char* gq = reinterpret_cast<const char*>(A.Qin + k0 * 4 * NP);
 #pragma unroll
-          for (int u = 0; u < ET; ++u) st<R>(gb + u * EB + (C::Y_RPP + t) * RB, R(0));
+      for (int t0 = 0; t0 < ET * NV; t0 += TG) {
+        const int t = t0 + q;
+        if (t < nE * NV) {
+          const int u = t / NV, w = t - u * NV;
+          cp_async16(gb + u * EB + C::X_Q * RB + w * 16, gq + 16 * t);
         }
       }
-    } else {
+      for (int t = q; t < nE * (GV + 2); t += TG) {
+        const int u = t / (GV + 2), w = t - u * (GV + 2);
+        char* eb = gb + u * EB;
+        if (w < GV) cp_async16(eb + C::O_GEO * RB + w * 16, reinterpret_cast<const char*>(A.geo + (k0 + u) * 12) + 16 * w);
+        else if (w == GV) cp_async16(eb + 28 * RB, A.nbr + (k0 + u) * 4);     // 4 neighbour ids
+        else cp_async4(eb + 28 * RB + 16, A.code + (k0 + u) * 4);             // 4 codes (bytes)
+      }
+      for (int t = q; t < nE * MP; t += TG) {
+        const int u = t / MP, b = t - u * MP;
+        cp_async_real<R>(gb + u * EB + (C::O_C + b) * RB, A.c2 + (k0 + u) * MP + b);
+      }
+#if BBW_PF
+      {  // L2 prefetch of the group's next batch (Q_in, residual, c^2)
+        const long long kn = A.elem_begin + (batch + (long long)gridDim.x * C::G) * ET;
+        if (kn < A.elem_end) {
+          const int ne = (int)((A.elem_end - kn) < ET ? (A.elem_end - kn) : ET);
+          const int nl = (ne * 4 * NP * RB + 127) / 128;
+          const char* pq = reinterpret_cast<const char*>(A.Qin + kn * 4 * NP);
+          const char* pr = reinterpret_cast<const char*>(A.res + kn * 4 * NP);
+          for (int l = q; l < nl; l += TG) {
+            prefetch_l2(pq + 128 * l);
+            if (A.mode == 0) prefetch_l2(pr + 128 * l);
+          }
+          if (q == 0) prefetch_l2(A.c2 + kn * MP);
+        }
+      }
+#endif
+      cp_async_wait_all();
+      sync();
+      for (int t = q; t < nE * 4; t += TG) {  // outward normal, |grad lambda_f|
+        const int u = t >> 2, f = t & 3;
+        char* sg = gb + u * EB + C::O_GEO * RB;
+        const R gx = ld<R>(sg + (3 * f) * RB), gy = ld<R>(sg + (3 * f + 1) * RB), gz = ld<R>(sg + (3 * f + 2) * RB);
+        const R gl = sqrt(gx * gx + gy * gy + gz * gz), il = R(1) / gl;
+        st<R>(sg + (12 + 4 * f) * RB, -gx * il);
+        st<R>(sg + (13 + 4 * f) * RB, -gy * il);
+        st<R>(sg + (14 + 4 * f) * RB, -gz * il);
+        st<R>(sg + (15 + 4 * f) * RB, gl);
+      }
+      for (int t = q; t < ET * 12; t += TG) {  // zero slots of the G'' (4) and Y'' (8) arrays
+        const int u = t / 12, z = t - u * 12;
+        const int off = z < 4 ? C::X_G + z * (NPM1 + 1) : C::Y_Y + (z - 4) * (NFP1 + 1);
+        st<R>(gb + u * EB + off * RB, R(0));
+      }
+      for (int t = q; t < nE * MP; t += TG) {  // c'' = c^2 / b!
+        const int u = t / MP, b = t - u * MP;
+        char* p = gb + u * EB + (C::O_C + b) * RB;
+        st<R>(p, ld<R>(p) * __ldg(invfacM + b));
+      }
+#else
       constexpr int NV = 4 * NP / VEC;
       using V = typename std::conditional<sizeof(R) == 8, double2, float4>::type;
       const V* gq = reinterpret_cast<const V*>(A.Qin + k0 * 4 * NP);
@@ -450,39 +649,48 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
         const int u = t >> 2, f = t & 3;
         int* nbs = reinterpret_cast<int*>(gb + u * EB + 28 * RB);
         nbs[f] = __ldg(A.nbr + (k0 + u) * 4 + f);
-        nbs[4 + f] = __ldg(A.code + (k0 + u) * 4 + f);
+        reinterpret_cast<uint8_t*>(nbs + 4)[f] = __ldg(A.code + (k0 + u) * 4 + f);
       }
       for (int t = q; t < nE * 4; t += TG) {  // grad lambda_f, outward normal, |grad lambda_f|
         const int u = t >> 2, f = t & 3;
         const R* g = A.geo + (k0 + u) * 12 + 3 * f;
         const R gx = __ldg(g), gy = __ldg(g + 1), gz = __ldg(g + 2);
         const R gl = sqrt(gx * gx + gy * gy + gz * gz), il = R(1) / gl;
-        char* s = gb + u * EB + C::O_GEO * RB;
-        st<R>(s + (3 * f) * RB, gx);
-        st<R>(s + (3 * f + 1) * RB, gy);
-        st<R>(s + (3 * f + 2) * RB, gz);
-        st<R>(s + (12 + 4 * f) * RB, -gx * il);
-        st<R>(s + (13 + 4 * f) * RB, -gy * il);
-        st<R>(s + (14 + 4 * f) * RB, -gz * il);
-        st<R>(s + (15 + 4 * f) * RB, gl);
+        char* sg = gb + u * EB + C::O_GEO * RB;
+        st<R>(sg + (3 * f) * RB, gx);
+        st<R>(sg + (3 * f + 1) * RB, gy);
+        st<R>(sg + (3 * f + 2) * RB, gz);
+        st<R>(sg + (12 + 4 * f) * RB, -gx * il);
+        st<R>(sg + (13 + 4 * f) * RB, -gy * il);
+        st<R>(sg + (14 + 4 * f) * RB, -gz * il);
+        st<R>(sg + (15 + 4 * f) * RB, gl);
       }
       for (int t = q; t < ET * 12; t += TG) {  // zero slots of the G'' (4) and Y'' (8) arrays
         const int u = t / 12, z = t - u * 12;
         const int off = z < 4 ? C::X_G + z * (NPM1 + 1) : C::Y_Y + (z - 4) * (NFP1 + 1);
         st<R>(gb + u * EB + off * RB, R(0));
       }
+      for (int t = q; t < nE * MP; t += TG) {
+        const int u = t / MP, b = t - u * MP;
+        st<R>(gb + u * EB + (C::O_C + b) * RB, __ldg(A.c2 + (k0 + u) * MP + b) * __ldg(invfacM + b));
+      }
+#endif
     }
-    for (int t = q; t < nE * MP; t += TG) {
-      const int u = t / MP, b = t - u * MP;
-      st<R>(gb + u * EB + (C::O_C + b) * RB, __ldg(A.c2 + (k0 + u) * MP + b) * __ldg(invfacM + b));
+    if (A.mode == 2) {
+      for (int t = q; t < nE * MP; t += TG) {
+        const int u = t / MP, b = t - u * MP;
+        st<R>(gb + u * EB + (C::O_C + b) * RB, __ldg(A.c2 + (k0 + u) * MP + b) * __ldg(invfacM + b));
+      }
     }
     sync();
     BBW_PT(0);
 
-    R qo[ET][4][KO];  // own Q_in coefficients (LSRK)
     R ru[ET][3][KO];  // own r_u (x/a! scaled until phase E)
+#if BBW_LSRK_REG
+    R qo[ET][4][KO];  // own Q_in coefficients (LSRK)
+#endif
     if (A.mode != 2) {
-      // ---- B0: own Q -> registers
+#if BBW_LSRK_REG
 #pragma unroll
       for (int u = 0; u < ET; ++u)
 #pragma unroll
@@ -492,6 +700,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
             const int a = q + TG * k;
             qo[u][c][k] = (a < NP) ? ld<R>(gb + u * EB + (C::X_Q + c * NP + a) * RB) : R(0);
           }
+#endif
       // ---- B1: fluxes, F' = |grad l_f| c! F.  All items of the thread are unrolled so the neighbour
       //      trace loads (L2) of every item are in flight together.
       {
@@ -508,7 +717,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
           for (int u = 0; u < ET; ++u) {
             const char* eb = gb + u * EB + C::X_Q * RB;
             const int* nbs = reinterpret_cast<const int*>(gb + u * EB + 28 * RB);
-            const int nb = nbs[f], code = nbs[4 + f];
+            const int nb = nbs[f], code = reinterpret_cast<const uint8_t*>(nbs + 4)[f];
             const R pm = ld<R>(eb + own), uxm = ld<R>(eb + own + NP * RB), uym = ld<R>(eb + own + 2 * NP * RB),
                     uzm = ld<R>(eb + own + 3 * NP * RB);
             R pp = -pm, uxp = uxm, uyp = uym, uzp = uzm;
@@ -632,10 +841,34 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
       }
       sync();
       BBW_PT(3);
+      // LSRK inputs of u (Q_in and the residual, L2 hits) are issued now and consumed in E
+#if BBW_LSRK_REG
+#define BBW_QU(u, d, k) qo[u][1 + d][k]
+#define BBW_SU(u, d, k) rs[u][1 + d][k]
+#else
+      R qu[ET][3][KO], su[ET][3][KO];
+      if (A.mode == 0) {
+#pragma unroll
+        for (int u = 0; u < ET; ++u)
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int k = 0; k < KO; ++k) {
+              const int a = q + TG * k;
+              const long long gi = (k0 + u) * 4 * NP + (1 + d) * NP + a;
+              const bool ok = u < nE && a < NP;
+              qu[u][d][k] = ok ? __ldg(A.Qin + gi) : R(0);
+              su[u][d][k] = ok ? __ldcs(A.res + gi) : R(0);
+            }
+      }
+#define BBW_QU(u, d, k) qu[u][d][k]
+#define BBW_SU(u, d, k) su[u][d][k]
+#endif
       // ---- D: lift layers j = 1..N: w'_j[d] = sum_s w'_{j-1}[d + e_s]
       static_for<1, N + 1, 1>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
         constexpr int m = N - j;
+        if constexpr (j == 1) zero_region<C>(gb, q, C::Y_RPP, C::NS);  // padded r'' rows (F', Y'' are dead)
         face_sum3<C, R, cnp2(m), C::X_L + layer_off(N, j - 1), NP, C::X_L + layer_off(N, j), NP, false>(
             gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(m), static_cast<const R*>(nullptr));
         sync();
@@ -643,17 +876,6 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
       });
       // ---- E: gather lifts; r''_p += S_p/(a!)^2 (+ source) -> smem; r_u = a! r''_u + S_u/a!; LSRK for u
       //      r''_p also goes to a zero-padded row copy (row stride N+1) in the dead face region for F
-      if constexpr (C::PAD) {
-        constexpr int NS = NFP * (N + 1);
-        const uint8_t* rowlen = tab + L.rowlen;
-        for (int t = q; t < NS; t += TG) {
-          const int row = t / (N + 1), a1 = t - row * (N + 1);
-          if (a1 >= (int)__ldg(rowlen + row)) {
-#pragma unroll
-            for (int u = 0; u < ET; ++u) st<R>(gb + u * EB + (C::Y_RPP + t) * RB, R(0));
-          }
-        }
-      }
       {
         const uint16_t* padoff = reinterpret_cast<const uint16_t*>(tab + L.padoff);
         R nrm[ET][12];  // outward normals of the group's elements, hoisted into registers
@@ -692,7 +914,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
               R rp = fma(sp, i2, ld<R>(eb + (C::O_RP + a) * RB));
               if (A.src && u < nE) rp = fma(A.src_amp * __ldg(A.src + kk * NP + a), i1, rp);
               st<R>(gb + u * EB + (C::O_RP + a) * RB, rp);
-              if constexpr (C::PAD) st<R>(gb + u * EB + C::Y_RPP * RB + pado, rp);
+              st<R>(gb + u * EB + C::Y_RPP * RB + pado, rp);
               const R r3[3] = {fma(ru[u][0][k], f1, sx * i1), fma(ru[u][1][k], f1, sy * i1),
                                fma(ru[u][2][k], f1, sz * i1)};
               if (u < nE) {
@@ -700,9 +922,9 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
                 for (int d = 0; d < 3; ++d) {
                   const long long gi = kk * 4 * NP + (1 + d) * NP + a;
                   if (A.mode == 0) {
-                    const R r = fma(A.rk_a, rs[u][1 + d][k], A.dt * r3[d]);
+                    const R r = fma(A.rk_a, BBW_SU(u, d, k), A.dt * r3[d]);
                     A.res[gi] = r;
-                    A.Qout[gi] = fma(A.rk_b, r, qo[u][1 + d][k]);
+                    A.Qout[gi] = fma(A.rk_b, r, BBW_QU(u, d, k));
                   } else {
                     A.Qout[gi] = r3[d];
                   }
@@ -721,6 +943,26 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
     constexpr int RES = wadg_result<C>();
 
     // ---- J: dp/dt = a!/N! b_N; outputs
+#if BBW_LSRK_REG
+#define BBW_QP(u, k) qo[u][0][k]
+#define BBW_SP(u, k) rs[u][0][k]
+#else
+    R qp[ET][KO], sp[ET][KO];
+    if (A.mode == 0) {
+#pragma unroll
+      for (int u = 0; u < ET; ++u)
+#pragma unroll
+        for (int k = 0; k < KO; ++k) {
+          const int a = q + TG * k;
+          const long long gi = (k0 + u) * 4 * NP + a;
+          const bool ok = u < nE && a < NP;
+          qp[u][k] = ok ? __ldg(A.Qin + gi) : R(0);
+          sp[u][k] = ok ? __ldcs(A.res + gi) : R(0);
+        }
+    }
+#define BBW_QP(u, k) qp[u][k]
+#define BBW_SP(u, k) sp[u][k]
+#endif
 #pragma unroll
     for (int k = 0; k < KO; ++k) {
       const int a = q + TG * k;
@@ -736,9 +978,9 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
           } else {
             const long long gi = kk * 4 * NP + a;
             if (A.mode == 0) {
-              const R r = fma(A.rk_a, rs[u][0][k], A.dt * dp);
+              const R r = fma(A.rk_a, BBW_SP(u, k), A.dt * dp);
               A.res[gi] = r;
-              A.Qout[gi] = fma(A.rk_b, r, qo[u][0][k]);
+              A.Qout[gi] = fma(A.rk_b, r, BBW_QP(u, k));
             } else {
               A.Qout[gi] = dp;
             }

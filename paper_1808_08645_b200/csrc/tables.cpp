@@ -193,20 +193,25 @@ HostTables build_tables(int N, int M, int RB) {
     W.put<int32_t>(L.csr_ptr, (int)iH.size(), t);
     if (t != lnp3(N) * lnp3(M)) throw std::runtime_error("CSR term count mismatch");
   }
-  // ROWDEC: rows of degree N+M in canonical order
+  // ROWDEC: rows of degree N+M ordered by g2 + g3 (then g3), so that a warp pass of the
+  // product takes rows of similar length
   {
     int r = 0;
-    for (int g3 = 0; g3 <= N + M; ++g3)
-      for (int g2 = 0; g2 <= N + M - g3; ++g2)
+    for (int s = 0; s <= N + M; ++s)
+      for (int g3 = 0; g3 <= s; ++g3) {
+        const int g2 = s - g3;
         W.put<uint32_t>(L.rowdec, r++, (uint32_t)g2 | ((uint32_t)g3 << 8) | ((uint32_t)rank3(N + M, 0, g2, g3) << 16));
+      }
   }
-  // PADOFF / ROWLEN: zero-padded row copy of degree-N arrays (row (a2,a3) at rowid*(N+1))
+  // PADOFF / ROWLEN: zero-padded row copy of degree-N arrays (row (a2,a3) at rowid*RS)
   {
     auto idx = indices3(N);
     for (size_t i = 0; i < idx.size(); ++i) {
       const int* a = idx[i].a;
       const int rowid = a[3] * (2 * N + 3 - a[3]) / 2 + a[2];
-      W.put<uint16_t>(L.padoff, (int)i, (uint16_t)((rowid * (N + 1) + a[1]) * RB));
+      const int VEC = 16 / RB, RS0 = (N + 1 + VEC - 1) / VEC * VEC;
+      const int RS = RS0 + ((RS0 / VEC) % 2 == 0 ? VEC : 0);  // row stride (StageCfg::RS): odd # of 16-B vectors
+      W.put<uint16_t>(L.padoff, (int)i, (uint16_t)((rowid * RS + a[1]) * RB));
     }
     int r = 0;
     for (int a3 = 0; a3 <= N; ++a3)
