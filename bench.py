@@ -311,7 +311,7 @@ def run_ours(args):
            "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
     s.close()
     if rank == 0 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(N, M, args.cpu_seconds)
+        out["cpu_baseline"] = cpu_baseline(N, M, args.cpu_seconds, extras=True)
     if rank == 0 and not args.no_sweep:
         out["sweep"] = sweep(args, dev)
     if rank == 0:
@@ -357,16 +357,21 @@ def sweep(args, dev):
         gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
         rows.append({"N": N, "M": M, "value": 4.0 * len(e) * Np * 5 / (ms / 1e3), "ms_per_step": ms,
                      "ns_per_element_stage": ms * 1e6 / (5 * len(e)), "hbm_frac": gbs / peaks["hbm_gbs"],
-                     "tflops": info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12})
+                     "tflops": info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12,
+                     "flops_per_element_stage": info["flops_per_stage"] / len(e),
+                     "bytes_per_element_stage": info["algorithmic_bytes_per_stage"] / len(e)})
         s.close()
-    Ns = np.array([r["N"] for r in rows if r["N"] >= 4], dtype=float)
-    ts = np.array([r["ns_per_element_stage"] for r in rows if r["N"] >= 4])
-    slope = float(np.polyfit(np.log(Ns), np.log(ts), 1)[0])
+    sel = [r for r in rows if r["N"] >= 4]
+    Ns = np.log(np.array([r["N"] for r in sel], dtype=float))
+    fit = lambda y: float(np.polyfit(Ns, np.log(np.array(y, dtype=float)), 1)[0])
     return {"workload": f"config3: Kuhn n={args.sweep_n} ({len(e):,} tets), M=N, c^2 k=8, fp64",
-            "rows": rows, "loglog_slope_time_per_element_N4to9": slope}
+            "rows": rows, "loglog_slope_time_per_element_N4to9": fit([r["ns_per_element_stage"] for r in sel]),
+            "loglog_slope_algorithmic_flops_N4to9": fit([r["flops_per_element_stage"] for r in sel]),
+            "loglog_slope_algorithmic_bytes_N4to9": fit([r["bytes_per_element_stage"] for r in sel]),
+            "paper_prediction": "O(N^4) per element for the WADG update at fixed M (P:1693); bytes O(N^3)"}
 
 
-def cpu_baseline(N, M, seconds):
+def cpu_baseline(N, M, seconds, extras=False):
     """The CPU oracle as it stands, timed on this host on a bounded sample."""
     import threadpoolctl
 
@@ -392,10 +397,45 @@ def cpu_baseline(N, M, seconds):
     Np = comb(N + 3, 3)
     info = threadpoolctl.threadpool_info()
     cores = max([i.get("num_threads", 1) for i in info] + [1])
-    return {"value": 4.0 * len(e) * Np * 5 * steps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{steps} LSRK45 step(s) of the oracle on a {len(e)}-tet Kuhn mesh (n={n}), N={N}, M={M}, "
-                      f"fp64 numpy/BLAS; table setup {setup:.1f}s excluded",
-            "cpu": os.uname().machine, "os_cpu_count": os.cpu_count()}
+    out = {"value": 4.0 * len(e) * Np * 5 * steps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{steps} LSRK45 step(s) of the oracle on a {len(e)}-tet Kuhn mesh (n={n}), N={N}, M={M}, "
+                     f"fp64 numpy/BLAS; table setup {setup:.1f}s excluded",
+           "cpu": os.uname().machine, "os_cpu_count": os.cpu_count()}
+    if extras:
+        out.update(cpu_extras())
+    return out
+
+
+def cpu_extras():
+    """SURVEY 8(d) oracle timings: total seconds of config 1 (48 tets, N=3, M=1, 10 LSRK45 steps with the
+    dt rule), and oracle DOF-stage/s on the 3072-tet mesh (n=8) at the (N, M) of configs 4 and 5 (one step
+    each, measured, not extrapolated)."""
+    from oracle.acoustic import AcousticOracle
+    from workloads import kuhn, media, states
+
+    v, e = kuhn.kuhn_mesh(2)
+    c2 = media.project_c2(v, e, media.c2_smooth(1.0), 1)
+    Q = states.random_state(len(e), 3)
+    t0 = time.perf_counter()
+    o = AcousticOracle(v, e, 3, 1, c2)
+    h = kuhn.min_height(v, e)
+    dt = 0.5 * h / (np.sqrt(1.5) * 16)
+    res = np.zeros_like(Q)
+    for i in range(10):
+        o.step(Q, res, i * dt, dt)
+    cfg1 = time.perf_counter() - t0
+    rates = {}
+    v, e = kuhn.kuhn_mesh(8)
+    for N, M in ((5, 3), (7, 4)):
+        c2 = media.project_c2(v, e, media.c2_smooth(1.0), M)
+        Q = states.random_state(len(e), N)
+        o = AcousticOracle(v, e, N, M, c2)
+        res = np.zeros_like(Q)
+        t0 = time.perf_counter()
+        o.step(Q, res, 0.0, 1e-4)
+        el = time.perf_counter() - t0
+        rates[f"N{N}M{M}"] = 4.0 * len(e) * comb(N + 3, 3) * 5 / el
+    return {"config1_total_seconds": cfg1, "oracle_dofstage_per_s_3072tets": rates}
 
 
 def run_reference(args):

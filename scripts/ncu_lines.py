@@ -45,7 +45,7 @@ def helper_lines(src):
         out = set()
         try:
             for i, ln in enumerate(open(src).read().splitlines(), 1):
-                if re.search(r"__forceinline__ (R ld|void st|void static_for|void cp_async|void prefetch_l2)\(", ln):
+                if re.search(r"__forceinline__ (R ld|void st|void static_for|void cp_async|void prefetch_l2|void ld_shared_vec_pred)\(", ln):
                     out.update(range(i, i + 6))
         except OSError:
             pass
