@@ -111,10 +111,16 @@ struct StageCfg {
   static constexpr int NPH1 = cnp3(N + M - 1);
   static constexpr int LEVSZ = NP4 + N + 1;
   static constexpr bool LAST_FROM_H = (M >= 1) && ((M - 1) % 2 == 0);
+  // ALIAS only when the WADG arrays would set the element's smem size (high N, M); otherwise the
+  // round-1 v3 layout (separate levels, ping-pong upward buffers A0/A1) is kept: measured ~2 % faster.
   static constexpr int W_H = O_X, W_P = W_H + NPH;
-  static constexpr int W_LEV = (M == 0 || LAST_FROM_H) ? W_P : (LEVSZ <= NPH ? W_H : W_P + NPH1);
-  static constexpr int WSIZE = cmax(cmax(W_LEV + LEVSZ, W_P + (M >= 1 ? NPH1 : 0)), W_H + NPH) - O_X;
-  static __host__ __device__ constexpr int lev(int n) { return W_LEV + lnp4(n - 1) + n + 1; }
+  static constexpr int WSIZE_V3 = 2 * NPH + NP4 + 2 * (NP + 1);
+  static constexpr bool ALIAS = WSIZE_V3 > XSIZE + YSIZE;
+  static constexpr int W_LEV = !ALIAS ? W_P + NPH : (M == 0 || LAST_FROM_H) ? W_P : (LEVSZ <= NPH ? W_H : W_P + NPH1);
+  static constexpr int W_A0 = W_LEV + NP4, W_A1 = W_A0 + NP + 1;  // !ALIAS only
+  static constexpr int WSIZE = !ALIAS ? WSIZE_V3
+                                      : cmax(cmax(W_LEV + LEVSZ, W_P + (M >= 1 ? NPH1 : 0)), W_H + NPH) - O_X;
+  static __host__ __device__ constexpr int lev(int n) { return ALIAS ? W_LEV + lnp4(n - 1) + n + 1 : W_LEV + lnp4(n - 1); }
   static constexpr int PER_E = rup(O_X + cmax(XSIZE + YSIZE, WSIZE), VEC);
   static constexpr int EB = PER_E * RB;  // element stride in bytes
   static constexpr int GB = ET * EB;     // group stride in bytes
@@ -185,9 +191,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 
 #ifndef BBW_PF
 #define BBW_PF 1
-#endif
-#ifndef BBW_PFN
-#define BBW_PFN 1
 #endif
 #ifndef BBW_LSRK_REG
 #define BBW_LSRK_REG 1
@@ -433,6 +436,15 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   }
   sync();
   BBW_PT(6);
+  if constexpr (!C::ALIAS) {
+    if (q == 0) {  // zero slots of the upward-sweep ping-pong buffers (may alias the padded rows read above)
+#pragma unroll
+      for (int u = 0; u < ET; ++u) {
+        st<R>(gb + C::W_A0 * RB + u * EB, R(0));
+        st<R>(gb + C::W_A1 * RB + u * EB, R(0));
+      }
+    }
+  }
   // G: M reductions N+M -> N (ping-pong H <-> P; the last lands in level N)
   static_for<N + M, N, -1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
@@ -451,10 +463,12 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
     sync();
     BBW_PT(7);
   }
-  // zero slots in front of levels 0..N-1 (read by the upward sweep); the region held h / P until now
-  if (q < N) {
+  // zero slots read by the upward sweep in front of levels 0..N-1 (ALIAS: the region held h / P until now)
+  if constexpr (C::ALIAS) {
+    if (q < N) {
 #pragma unroll
-    for (int u = 0; u < ET; ++u) st<R>(gb + (C::lev(q) - 1) * RB + u * EB, R(0));
+      for (int u = 0; u < ET; ++u) st<R>(gb + (C::lev(q) - 1) * RB + u * EB, R(0));
+    }
   }
   // H: downward reductions level n -> n-1
   static_for<N, 0, -1>([&](auto nc) {
@@ -466,7 +480,9 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   // I: upward, in place: b_n[a] = sum_j b_{n-1}[a - e_j] + gam_n/(a!)^2 u_n[a] overwrites u_n (b_0 = gam_0 u_0)
   static_for<1, N + 1, 1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
-    constexpr int SRC = C::lev(n - 1) - 1;  // UPW offsets are (rank + 1) * RB, 0 = the zero slot
+    // UPW offsets are (rank + 1) * RB, 0 = the zero slot; b_n -> level n in place (ALIAS) or A_{n%2}
+    constexpr int SRC = C::ALIAS ? C::lev(n - 1) - 1 : ((n % 2 == 1) ? C::W_A0 : C::W_A1);
+    constexpr int DST = C::ALIAS ? C::lev(n) : ((n % 2 == 1) ? C::W_A1 : C::W_A0) + 1;
     const R gn = A.gam[n];
     if constexpr (n == 1) {
       // degree 1: every a has exactly one valid a - e_j (= the single b_0), weight 1/(a!)^2 = 1
@@ -475,8 +491,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
 #pragma unroll
         for (int u = 0; u < ET; ++u) {
           const R b0 = g0 * ld<R>(gb + C::lev(0) * RB + u * EB);
-          char* d = gb + (C::lev(1) + i) * RB + u * EB;
-          st<R>(d, fma(gn, ld<R>(d), b0));
+          st<R>(gb + (DST + i) * RB + u * EB, fma(gn, ld<R>(gb + (C::lev(1) + i) * RB + u * EB), b0));
         }
     } else {
       const uint8_t* up = tab + L.upw + 16 * upw_off(n);
@@ -496,16 +511,15 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         const char* p1 = gb + o[k].y + SRC * RB;
         const char* p2 = gb + o[k].z + SRC * RB;
         const char* p3 = gb + o[k].w + SRC * RB;
-        char* d = gb + (C::lev(n) + cmin(i, CNT - 1)) * RB;
         R v[ET];
 #pragma unroll
         for (int u = 0; u < ET; ++u) {
           v[u] = (ld<R>(p0 + u * EB) + ld<R>(p1 + u * EB)) + (ld<R>(p2 + u * EB) + ld<R>(p3 + u * EB));
-          v[u] = fma(w[k], ld<R>(d + u * EB), v[u]);
+          v[u] = fma(w[k], ld<R>(gb + (C::lev(n) + cmin(i, CNT - 1)) * RB + u * EB), v[u]);
         }
         if ((CNT % TG == 0) || i < CNT) {
 #pragma unroll
-          for (int u = 0; u < ET; ++u) st<R>(d + u * EB, v[u]);
+          for (int u = 0; u < ET; ++u) st<R>(gb + (DST + i) * RB + u * EB, v[u]);
         }
       }
     }
@@ -516,7 +530,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
 
 template <class C>
 __host__ __device__ constexpr int wadg_result() {
-  return C::lev(C::N);
+  return C::ALIAS ? C::lev(C::N) : ((C::N % 2 == 1) ? C::W_A1 + 1 : C::W_A0 + 1);
 }
 
 template <class C, typename R>
@@ -544,14 +558,14 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
   const uint16_t* nbrvol = reinterpret_cast<const uint16_t*>(tab + L.nbrvol);
   const uint16_t* nbrface = reinterpret_cast<const uint16_t*>(tab + L.nbrface);
 
-  int nbn = -1;  // lane t < 4 ET: neighbour id (face t % 4, element t / 4) of the group's next batch
   const long long nelem = A.elem_end - A.elem_begin;
   const long long nbatch = (nelem + ET - 1) / ET;
   for (long long batch = (long long)blockIdx.x * C::G + grp; batch < nbatch; batch += (long long)gridDim.x * C::G) {
     const long long k0 = A.elem_begin + batch * ET;
     long long pt_prev = clock64();
     (void)pt_prev;
-    const int nE = (int)((A.elem_end - k0) < ET ? (A.elem_end - k0) : ET);
+    // valid elements of the batch (compile-time 1 for ET == 1: every batch start is < elem_end)
+    const int nE = (ET == 1) ? 1 : (int)((A.elem_end - k0) < ET ? (A.elem_end - k0) : ET);
 
     // ---- A: loads (Q, geometry, c'' -> smem via cp.async; the residual is only prefetched into L2
     //      here and read in phases D and J, so no registers are held across the WADG phases)
@@ -623,9 +637,6 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
             if (A.mode == 0) prefetch_l2(pr + 128 * l);
           }
           if (q == 0) prefetch_l2(A.c2 + kn * MP);
-#if BBW_PFN
-          if (q < 4 * ne) nbn = __ldg(A.nbr + kn * 4 + q);  // the next batch's neighbours (prefetched in F)
-#endif
         }
       }
 #endif
@@ -952,22 +963,6 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
       BBW_PT(5);
     }
 
-#if BBW_PF && BBW_PFN
-    // L2 prefetch of the Q_in blocks of the next batch's neighbours (their face traces are read in
-    // B1 of the next batch; Morton-distant neighbours would otherwise come from DRAM with B1 waiting)
-    if (A.mode != 2) {
-      constexpr int NLQ = (4 * NP * RB + 127) / 128;
-#pragma unroll 1
-      for (int t = 0; t < 4 * ET; ++t) {
-        const int nb = __shfl_sync(0xffffffffu, nbn, t);
-        if (nb >= 0) {
-          const char* pq = reinterpret_cast<const char*>(A.Qin + (long long)nb * 4 * NP);
-          for (int l = q; l < NLQ; l += TG) prefetch_l2(pq + 128 * l);
-        }
-      }
-      nbn = -1;
-    }
-#endif
     // ---- F-I: WADG multiply + telescoping projection of r_p
     wadg_phases<C, R>(gb, q, A, sync, pt_prev);
     constexpr int RES = wadg_result<C>();
