@@ -22,7 +22,7 @@ __host__ __device__ constexpr int al16(int x) { return (x + 15) & ~15; }
 struct TabLayout {
   // byte offsets of the sections
   int vg, ve, red, upw, lg, trired, triele, fnode, nbrvol, nbrface, csr_ptr, csr_terms, rowdec, padoff, rowlen;
-  int s_invfacN, s_facN, s_invfac2N, s_outN, s_invfacM, s_post, s_invfacNm1, s_cfac, s_invf2, s_cf2;
+  int s_invfacN, s_facN, s_invfac2N, s_outN, s_invfacM, s_post, s_invfacNm1, s_cfac, s_invf2, s_cf2, s_rowpost;
   int total;
 };
 
@@ -41,7 +41,8 @@ struct TabLayout {
 // PADOFF [Np(N)]           uint16: byte offset of a in the zero-padded row copy (row stride RS)
 // ROWLEN [Np2(N)]          uint8: length N - a2 - a3 + 1 of row (a2, a3) of degree N
 // scale arrays (reals): 1/a!, a!, 1/(a!)^2, a!/N! (deg N); 1/b! (deg M); (g!)^2 N! M!/(N+M)! (deg N+M);
-//                       1/b! (deg N-1); c!, 1/(d!)^2 (deg N-1), (c!)^2 (face, deg N)
+//                       1/b! (deg N-1); c!, 1/(d!)^2 (deg N-1), (c!)^2 (face, deg N);
+//                       ROWPOST [Np2(N+M)] N!M!/(N+M)! (g2!)^2 (g3!)^2 per product output row (ROWDEC order)
 __host__ __device__ constexpr TabLayout tab_layout(int N, int M, int RB) {
   TabLayout L{};
   int o = 0;
@@ -70,6 +71,7 @@ __host__ __device__ constexpr TabLayout tab_layout(int N, int M, int RB) {
   L.s_cfac = o;     o = al16(o + RB * lnp2(N));
   L.s_invf2 = o;    o = al16(o + RB * lnp2(N - 1));
   L.s_cf2 = o;      o = al16(o + RB * lnp2(N));
+  L.s_rowpost = o;  o = al16(o + RB * lnp2(N + M));
   L.total = o;
   return L;
 }

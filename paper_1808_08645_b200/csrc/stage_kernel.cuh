@@ -213,6 +213,13 @@ __device__ __forceinline__ void ld_shared_vec_pred(R* x, unsigned addr, bool p) 
   }
 }
 
+// (x!)^2 as a compile-time constant (exact integer factorial, one rounding)
+__host__ __device__ constexpr double fact2c(int x) {
+  double f = 1.0;
+  for (int i = 2; i <= x; ++i) f *= i;
+  return f * f;
+}
+
 template <typename R>
 __device__ __forceinline__ R ld(const char* p) { return *reinterpret_cast<const R*>(p); }
 template <typename R>
@@ -303,6 +310,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   const int* csr_ptr = reinterpret_cast<const int*>(tab + L.csr_ptr);
   const uint32_t* csr = reinterpret_cast<const uint32_t*>(tab + L.csr_terms);
   const R* post = reinterpret_cast<const R*>(tab + L.s_post);
+  const R* rowpost = reinterpret_cast<const R*>(tab + L.s_rowpost);
   const ushort4* red = reinterpret_cast<const ushort4*>(tab + L.red);
 
   // F: h'_g = post_g * sum_{a+b=g} r''_a c''_b, output-row stationary: for output row (g2,g3) of
@@ -376,6 +384,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
       const int rho = q + TG * k;
       const bool act = rho < NR;
       const uint32_t d = __ldg(rowdec + (act ? rho : NR - 1));
+      const R rowf = __ldg(rowpost + (act ? rho : NR - 1));
       const int g2 = d & 0xFF, g3 = (d >> 8) & 0xFF, gs = (int)(d >> 16);
       const int smin = __reduce_min_sync(0xffffffffu, act ? g2 + g3 : 4 * (N + M));
       // rowid(a2, a3) = a3 (2N+3-a3)/2 + a2 at a = G - B: rid0 + b3 g3 - b3 (2N+3+b3)/2 - b2
@@ -421,13 +430,31 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         });
       });
       if (act) {
+        // h'_g = N!M!/(N+M)! (g!)^2 h''_g with g = (lg-1-x, x, g2, g3): the row factor comes from
+        // ROWPOST, (x!)^2 is a compile-time constant and (g0!)^2 a running product over x = lg-1 .. 0
+        // (no per-output table load)
         const int lg = N + M - g2 - g3 + 1;
+        if constexpr (N + M <= 12) {
+          R P = rowf, T = R(lg - (N + M));
+          static_for<N + M, -1, -1>([&](auto xc) {
+            constexpr int x = decltype(xc)::value;
+            if (x < lg) {
 #pragma unroll
-        for (int x = 0; x <= N + M; ++x) {
-          if (x < lg) {
-            const R s = __ldg(post + gs + x);
+              for (int u = 0; u < ET; ++u)
+                st<R>(gb + (C::W_H + gs + x) * RB + u * EB, acc[u][x] * (R(fact2c(x)) * P));
+            }
+            const R Tc = T > R(1) ? T : R(1);  // (g0 + 1)^2 for x < lg, 1 above the row
+            P *= Tc * Tc;
+            T += R(1);
+          });
+        } else {  // long rows (N+M > 12): the per-output table is faster (measured at N = M = 9)
 #pragma unroll
-            for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + gs + x) * RB + u * EB, acc[u][x] * s);
+          for (int x = 0; x <= N + M; ++x) {
+            if (x < lg) {
+              const R sp = __ldg(post + gs + x);
+#pragma unroll
+              for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + gs + x) * RB + u * EB, acc[u][x] * sp);
+            }
           }
         }
       }
@@ -549,7 +576,6 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
   const uint8_t* tab = A.tab;
   const R* invfacN = reinterpret_cast<const R*>(tab + L.s_invfacN);
   const R* facN = reinterpret_cast<const R*>(tab + L.s_facN);
-  const R* invfac2N = reinterpret_cast<const R*>(tab + L.s_invfac2N);
   const R* outN = reinterpret_cast<const R*>(tab + L.s_outN);
   const R* invfacM = reinterpret_cast<const R*>(tab + L.s_invfacM);
   const R* invfacNm1 = reinterpret_cast<const R*>(tab + L.s_invfacNm1);
@@ -715,61 +741,38 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
     R qo[ET][4][KO];  // own Q_in coefficients (LSRK)
 #endif
     if (A.mode != 2) {
-#if BBW_LSRK_REG
+      // ---- B1a: neighbour face traces of every flux item are requested first (L2 / DRAM latency),
+      //      then B2 runs while they are in flight, then B1b forms the fluxes.
+      constexpr int NI1 = 4 * NFP, K1 = (NI1 + TG - 1) / TG;
+      R tpp[K1][ET], tux[K1][ET], tuy[K1][ET], tuz[K1][ET];
+      int town[K1];
 #pragma unroll
-      for (int u = 0; u < ET; ++u)
+      for (int k = 0; k < K1; ++k) {
+        const int t = q + TG * k;
+        const bool act = (NI1 % TG == 0) || t < NI1;
+        const int tc = act ? t : 0;
+        const int f = tc / NFP, i = tc - f * NFP;
+        town[k] = __ldg(fnode + f * NFP + i);
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int k = 0; k < KO; ++k) {
-            const int a = q + TG * k;
-            qo[u][c][k] = (a < NP) ? ld<R>(gb + u * EB + (C::X_Q + c * NP + a) * RB) : R(0);
-          }
-#endif
-      // ---- B1: fluxes, F' = |grad l_f| c! F.  All items of the thread are unrolled so the neighbour
-      //      trace loads (L2) of every item are in flight together.
-      {
-        constexpr int NI = 4 * NFP, K1 = (NI + TG - 1) / TG;
-#pragma unroll
-        for (int k = 0; k < K1; ++k) {
-          const int t = q + TG * k;
-          const bool act = (NI % TG == 0) || t < NI;
-          const int tc = act ? t : 0;
-          const int f = tc / NFP, i = tc - f * NFP;
-          const int own = __ldg(fnode + f * NFP + i);
-          const R cs = __ldg(cfac + i);
-#pragma unroll
-          for (int u = 0; u < ET; ++u) {
-            const char* eb = gb + u * EB + C::X_Q * RB;
-            const int* nbs = reinterpret_cast<const int*>(gb + u * EB + 28 * RB);
-            const int nb = nbs[f], code = reinterpret_cast<const uint8_t*>(nbs + 4)[f];
-            const R pm = ld<R>(eb + own), uxm = ld<R>(eb + own + NP * RB), uym = ld<R>(eb + own + 2 * NP * RB),
-                    uzm = ld<R>(eb + own + 3 * NP * RB);
-            R pp = -pm, uxp = uxm, uyp = uym, uzp = uzm;
-            if (act && u < nE) {
-              if (nb >= 0) {
-                const int vol = __ldg(nbrvol + code * NFP + i);
-                const R* qn = A.Qin + (long long)nb * 4 * NP + vol;
-                pp = __ldg(qn);
-                uxp = __ldg(qn + NP);
-                uyp = __ldg(qn + 2 * NP);
-                uzp = __ldg(qn + 3 * NP);
-              } else if (nb < -1) {
-                const int fi = __ldg(nbrface + (code % 6) * NFP + i);
-                const R* gh = A.ghost + (long long)(-2 - nb) * 4 * NFP + fi;
-                pp = gh[0];
-                uxp = gh[NFP];
-                uyp = gh[2 * NFP];
-                uzp = gh[3 * NFP];
-              }
-            }
-            const char* gs = gb + u * EB + (C::O_GEO + 12 + 4 * f) * RB;
-            const R nx = ld<R>(gs), ny = ld<R>(gs + RB), nz = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * cs;
-            const R jp = pp - pm;
-            const R jun = nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
-            if (act) {
-              st<R>(gb + u * EB + (C::Y_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));
-              st<R>(gb + u * EB + (C::Y_F + (2 * f + 1) * NFP + i) * RB, R(0.5) * sc * (A.tau_u * jun - jp));
+        for (int u = 0; u < ET; ++u) {
+          const int* nbs = reinterpret_cast<const int*>(gb + u * EB + 28 * RB);
+          const int nb = nbs[f], code = reinterpret_cast<const uint8_t*>(nbs + 4)[f];
+          tpp[k][u] = tux[k][u] = tuy[k][u] = tuz[k][u] = R(0);
+          if (act && u < nE) {
+            if (nb >= 0) {
+              const int vol = __ldg(nbrvol + code * NFP + i);
+              const R* qn = A.Qin + (long long)nb * 4 * NP + vol;
+              tpp[k][u] = __ldg(qn);
+              tux[k][u] = __ldg(qn + NP);
+              tuy[k][u] = __ldg(qn + 2 * NP);
+              tuz[k][u] = __ldg(qn + 3 * NP);
+            } else if (nb < -1) {
+              const int fi = __ldg(nbrface + (code % 6) * NFP + i);
+              const R* gh = A.ghost + (long long)(-2 - nb) * 4 * NFP + fi;
+              tpp[k][u] = gh[0];
+              tux[k][u] = gh[NFP];
+              tuy[k][u] = gh[2 * NFP];
+              tuz[k][u] = gh[3 * NFP];
             }
           }
         }
@@ -809,6 +812,46 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
           }
         }
       }
+      // ---- B1b: fluxes, F' = |grad l_f| c! F  (boundary: p+ = -p, u+ = u, R11)
+#pragma unroll
+      for (int k = 0; k < K1; ++k) {
+        const int t = q + TG * k;
+        const bool act = (NI1 % TG == 0) || t < NI1;
+        const int tc = act ? t : 0;
+        const int f = tc / NFP, i = tc - f * NFP;
+        const int own = town[k];
+        const R cs = __ldg(cfac + i);
+#pragma unroll
+        for (int u = 0; u < ET; ++u) {
+          const char* eb = gb + u * EB + C::X_Q * RB;
+          const int nb = reinterpret_cast<const int*>(gb + u * EB + 28 * RB)[f];
+          const R pm = ld<R>(eb + own), uxm = ld<R>(eb + own + NP * RB), uym = ld<R>(eb + own + 2 * NP * RB),
+                  uzm = ld<R>(eb + own + 3 * NP * RB);
+          const bool bnd = (nb == -1) || !(act && u < nE);
+          const R pp = bnd ? -pm : tpp[k][u], uxp = bnd ? uxm : tux[k][u], uyp = bnd ? uym : tuy[k][u],
+                  uzp = bnd ? uzm : tuz[k][u];
+          const char* gs = gb + u * EB + (C::O_GEO + 12 + 4 * f) * RB;
+          const R nx = ld<R>(gs), ny = ld<R>(gs + RB), nz = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * cs;
+          const R jp = pp - pm;
+          const R jun = nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
+          if (act) {
+            st<R>(gb + u * EB + (C::Y_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));
+            st<R>(gb + u * EB + (C::Y_F + (2 * f + 1) * NFP + i) * RB, R(0.5) * sc * (A.tau_u * jun - jp));
+          }
+        }
+      }
+#if BBW_LSRK_REG
+      // ---- B0: own Q -> registers (LSRK)
+#pragma unroll
+      for (int u = 0; u < ET; ++u)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int k = 0; k < KO; ++k) {
+            const int a = q + TG * k;
+            qo[u][c][k] = (a < NP) ? ld<R>(gb + u * EB + (C::X_Q + c * NP + a) * RB) : R(0);
+          }
+#endif
       sync();
       BBW_PT(1);
       // ---- C1: r''_c[a] = -sum_j g''_c[a - e_j]  (p -> smem R_p, u -> registers)
@@ -920,7 +963,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
             R lm[4];
 #pragma unroll
             for (int f = 0; f < 4; ++f) lm[f] = lam_s[(e.z >> (8 * f)) & 0xFF];
-            const R i1 = __ldg(invfacN + a), i2 = __ldg(invfac2N + a), f1 = __ldg(facN + a);
+            const R i1 = __ldg(invfacN + a), i2 = i1 * i1, f1 = __ldg(facN + a);  // 1/a!, 1/(a!)^2, a!
             const int pado = __ldg(padoff + a);
 #pragma unroll
             for (int u = 0; u < ET; ++u) {

@@ -2,8 +2,12 @@
 #include "tables.hpp"
 #include "layout.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace bbw {
 
@@ -66,6 +70,138 @@ struct Writer {
     }
   }
 };
+}  // namespace
+
+
+// ---- product row order (ROWDEC).  Rows (g2, g3) of degree N+M are sorted by g2 + g3 (so one warp
+// pass holds rows of similar length); inside each warp pass the lane order is
+// then chosen to minimise shared-memory wavefronts of the pass's accesses under the bank model that
+// reproduces ncu's counts (profiles/r1_v4_*): 16-B row loads per c''-row (8 lanes per wavefront,
+// 16-B units mod 8) and the scaled output stores (8-B: 16 lanes per wavefront, units mod 16; 4-B: 32
+// lanes, units mod 32).  Deterministic annealing (fixed seed); any order is correct.
+namespace {
+// cost of one quarter-warp (loads) or half-warp (stores): max over bank units of distinct addresses
+inline int group_cost(const int* addr, int n, int mod) {
+  int best = 0;
+  for (int a = 0; a < n; ++a) {
+    if (addr[a] < 0) continue;
+    int c = 0;
+    bool dup = false;
+    for (int b = 0; b < a; ++b)
+      if (addr[b] == addr[a]) { dup = true; break; }
+    if (dup) continue;
+    for (int b = 0; b < n; ++b) {
+      if (addr[b] < 0 || addr[b] % mod != addr[a] % mod) continue;
+      bool seen = false;
+      for (int e = 0; e < b; ++e)
+        if (addr[e] == addr[b]) { seen = true; break; }
+      if (!seen) ++c;
+    }
+    best = std::max(best, c);
+  }
+  return best;
+}
+
+std::vector<std::pair<int, int>> product_row_order_uncached(int N, int M, int RB) {
+  const int VEC = 16 / RB, RS0 = (N + 1 + VEC - 1) / VEC * VEC, RS = RS0 + ((RS0 / VEC) % 2 == 0 ? VEC : 0);
+  const int NFP = (N + 1) * (N + 2) / 2, SL = RB == 8 ? 16 : 32, SMOD = RB == 8 ? 16 : 32;
+  std::vector<std::pair<int, int>> G, Bs, out;
+  for (int s = 0; s <= N + M; ++s)
+    for (int g3 = 0; g3 <= s; ++g3) G.push_back({s - g3, g3});
+  for (int b3 = 0; b3 <= M; ++b3)
+    for (int b2 = 0; b2 <= M - b3; ++b2) Bs.push_back({b2, b3});
+  const int NR = (int)G.size(), NB = (int)Bs.size();
+  uint64_t st = 0x9E3779B97F4A7C15ull;
+  auto rnd = [&]() { st ^= st << 13; st ^= st >> 7; st ^= st << 17; return st; };
+  for (int r0 = 0; r0 < NR; r0 += 32) {  // one warp pass (a TG = 64 group is two warps)
+    int rr[32];
+    for (int l = 0; l < 32; ++l) rr[l] = r0 + l < NR ? r0 + l : -1;
+    int smin = 1 << 20;
+    for (int l = 0; l < 32; ++l)
+      if (rr[l] >= 0) smin = std::min(smin, G[rr[l]].first + G[rr[l]].second);
+    // per row r (of this pass) and c''-row B: 16-B unit of its input row (-2: no lane; NFP row = zeros)
+    std::vector<int> nvec(NB, 0);
+    std::vector<char> anyv(NB, 0);
+    auto unit = [&](int r, int b) {
+      if (r < 0) return -1;
+      const int a2 = G[r].first - Bs[b].first, a3 = G[r].second - Bs[b].second;
+      const bool valid = a2 >= 0 && a3 >= 0 && a2 + a3 <= N;
+      return (valid ? a3 * (2 * N + 3 - a3) / 2 + a2 : NFP) * RS / VEC;
+    };
+    for (int b = 0; b < NB; ++b) {
+      for (int l = 0; l < 32; ++l) {
+        if (rr[l] < 0) continue;
+        const int a2 = G[rr[l]].first - Bs[b].first, a3 = G[rr[l]].second - Bs[b].second;
+        if (a2 >= 0 && a3 >= 0 && a2 + a3 <= N) anyv[b] = 1;
+      }
+      const int lamax = std::min(N + 1, N + 1 - smin + Bs[b].first + Bs[b].second);
+      nvec[b] = anyv[b] ? (lamax + VEC - 1) / VEC : 0;
+    }
+    auto qcost = [&](int q0) {  // loads of lanes q0..q0+7 over every c''-row and vector
+      int c = 0, ad[8];
+      for (int b = 0; b < NB; ++b) {
+        if (!nvec[b]) continue;
+        for (int l = 0; l < 8; ++l) ad[l] = unit(rr[q0 + l], b);
+        for (int v = 0; v < nvec[b]; ++v) {
+          int av[8];
+          for (int l = 0; l < 8; ++l) av[l] = ad[l] < 0 ? -1 : ad[l] + v;
+          c += group_cost(av, 8, 8);
+        }
+      }
+      return c;
+    };
+    auto hcost = [&](int h0) {  // output stores of lanes h0..h0+SL-1 over every x
+      int c = 0, ad[32];
+      for (int x = 0; x <= N + M; ++x) {
+        for (int l = 0; l < SL; ++l) {
+          const int r = rr[h0 + l];
+          ad[l] = (r < 0 || x >= N + M + 1 - G[r].first - G[r].second) ? -1 : rank3(N + M, 0, G[r].first, G[r].second) + x;
+        }
+        c += group_cost(ad, SL, SMOD);
+      }
+      return c;
+    };
+    int qc[4], hc[2], cur = 0;
+    for (int g = 0; g < 4; ++g) cur += (qc[g] = qcost(8 * g));
+    for (int g = 0; g < 32 / SL; ++g) cur += (hc[g] = hcost(SL * g));
+    int best = cur, bestrr[32];
+    std::copy(rr, rr + 32, bestrr);
+    double T = 3.0;
+    const int iters = NB > 20 ? 600 : 2000;
+    for (int it = 0; it < iters; ++it) {
+      const int i = (int)(rnd() % 32), j = (int)(rnd() % 32);
+      if (i / 8 == j / 8 || (rr[i] < 0 && rr[j] < 0)) continue;  // same quarter: loads unchanged
+      std::swap(rr[i], rr[j]);
+      const int qi = qcost(8 * (i / 8)), qj = qcost(8 * (j / 8));
+      const int hi = hcost(SL * (i / SL)), hj = (i / SL == j / SL) ? hi : hcost(SL * (j / SL));
+      const int c = cur - qc[i / 8] - qc[j / 8] + qi + qj - hc[i / SL] + hi - (i / SL == j / SL ? 0 : hc[j / SL] - hj);
+      if (c <= cur || (double)(rnd() % 1000000) / 1e6 < std::exp(-(c - cur) / T)) {
+        cur = c;
+        qc[i / 8] = qi;
+        qc[j / 8] = qj;
+        hc[i / SL] = hi;
+        hc[j / SL] = hj;
+        if (c < best) best = c, std::copy(rr, rr + 32, bestrr);
+      } else {
+        std::swap(rr[i], rr[j]);
+      }
+      T = std::max(0.05, T * 0.997);
+    }
+    for (int l = 0; l < 32; ++l)
+      if (bestrr[l] >= 0) out.push_back(G[bestrr[l]]);
+  }
+  return out;
+}
+
+std::vector<std::pair<int, int>> product_row_order(int N, int M, int RB) {
+  static std::mutex mu;
+  static std::map<int, std::vector<std::pair<int, int>>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const int key = (N * 16 + M) * 16 + RB;
+  auto it = cache.find(key);
+  if (it == cache.end()) it = cache.emplace(key, product_row_order_uncached(N, M, RB)).first;
+  return it->second;
+}
 }  // namespace
 
 HostTables build_tables(int N, int M, int RB) {
@@ -193,13 +329,14 @@ HostTables build_tables(int N, int M, int RB) {
     W.put<int32_t>(L.csr_ptr, (int)iH.size(), t);
     if (t != lnp3(N) * lnp3(M)) throw std::runtime_error("CSR term count mismatch");
   }
-  // ROWDEC: rows of degree N+M ordered by g2 + g3 (then g3), so that a warp pass of the
-  // product takes rows of similar length
+  // ROWDEC / ROWPOST: rows of degree N+M in warp passes of similar g2 + g3, lane order chosen
+  // against shared-memory bank conflicts (product_row_order)
   {
     int r = 0;
-    for (int s = 0; s <= N + M; ++s)
-      for (int g3 = 0; g3 <= s; ++g3) {
-        const int g2 = s - g3;
+    for (const auto& gg : product_row_order(N, M, RB)) {
+        const int g2 = gg.first, g3 = gg.second;
+        const long double f = lfact(g2) * lfact(g3);
+        W.real(L.s_rowpost, r, f * f * lfact(N) * lfact(M) / lfact(N + M), RB);
         W.put<uint32_t>(L.rowdec, r++, (uint32_t)g2 | ((uint32_t)g3 << 8) | ((uint32_t)rank3(N + M, 0, g2, g3) << 16));
       }
   }
