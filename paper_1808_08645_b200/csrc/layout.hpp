@@ -30,7 +30,7 @@ struct TabLayout {
 // VE   [Np(N)]              ushort4: (rank_{N-1}(a-e_j)+1)*RB or 0        (volume elevation, zero slot)
 // RED  [n=1..N+M][Np(n-1)]  ushort4: rank_n(b+e_j)*RB                     (reductions n -> n-1)
 // UPW  [n=1..N][Np(n)]      16 B: ushort4 (rank_{n-1}(a-e_j)+1)*RB or 0, real weight 1/(a!)^2
-// LG   [Np(N)]              16 B: ushort4 layer byte offsets per face, uchar4 layer index a_f
+// LG   [Np(N)]              ushort4: byte offset of coefficient a in lift layer a_f of face f (0..3)
 // TRIRED [m=0..N-1][Np2(m)] ushort4: trirank_{m+1}(c+e_s)*RB, s = 0..2      (face reductions)
 // TRIELE [Np2(N)]           ushort4: (trirank_{N-1}(c-e_s)+1)*RB or 0     (face elevation)
 // FNODE  [4][Np2(N)]        uint16: rank_N of face node i of face f, times RB
@@ -50,7 +50,7 @@ __host__ __device__ constexpr TabLayout tab_layout(int N, int M, int RB) {
   L.ve = o;       o = al16(o + 8 * lnp3(N));
   L.red = o;      o = al16(o + 8 * lnp4(N + M - 1));
   L.upw = o;      o = al16(o + 16 * (lnp4(N) - 1));
-  L.lg = o;       o = al16(o + 16 * lnp3(N));
+  L.lg = o;       o = al16(o + 8 * lnp3(N));
   L.trired = o;   o = al16(o + 8 * lnp3(N - 1));
   L.triele = o;   o = al16(o + 8 * lnp2(N));
   L.fnode = o;    o = al16(o + 2 * 4 * lnp2(N));

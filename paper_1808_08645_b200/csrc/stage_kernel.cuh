@@ -220,6 +220,22 @@ __host__ __device__ constexpr double fact2c(int x) {
   return f * f;
 }
 
+// unpredicated 16-B shared load into x[0..VEC) (opaque to the compiler, so x stays in registers)
+template <typename R, int OFF>
+__device__ __forceinline__ void ld_shared_vec(R* x, unsigned addr) {
+  if constexpr (sizeof(R) == 8) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];\n" : "+d"(x[0]), "+d"(x[1]) : "r"(addr), "n"(OFF));
+  } else {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];\n"
+                 : "+f"(x[0]), "+f"(x[1]), "+f"(x[2]), "+f"(x[3])
+                 : "r"(addr), "n"(OFF));
+  }
+}
+
+#ifndef BBW_PROD_SWITCH
+#define BBW_PROD_SWITCH 0  // measured 4-6 % slower than the predicated loads + branches
+#endif
+
 template <typename R>
 __device__ __forceinline__ R ld(const char* p) { return *reinterpret_cast<const R*>(p); }
 template <typename R>
@@ -260,34 +276,64 @@ __device__ __forceinline__ void sum4_phase(char* gb, int q, const ushort4* __res
   }
 }
 
-// dst_ff[i] = scale(i) * sum_s src_ff[off_s(i)] (3 terms) for the 8 face/flux arrays, ET elements
-template <class C, typename R, int CNT, int SRC, int SSTRIDE, int DST, int DSTRIDE, bool SCALED>
+// dst_ff[i] = scale(i) * sum_s src_ff[off_s(i)] (3 terms) for the 8 face/flux arrays, ET elements.
+// Small triangles (the top lift layers) split the 8 arrays over NG lane groups (NG * CNT <= 32), so a
+// warp issues 24/NG instead of 24 loads for them; each lane still loads its table entry once.
+template <class C, typename R, int CNT, int SRC, int SSTRIDE, int DST, int DSTRIDE, bool SCALED, int SNUM = 1,
+          int SDEN = 1>
 __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __restrict__ tab, const R* __restrict__ scale) {
-  constexpr int K = (CNT + C::TG - 1) / C::TG;
-  ushort4 o[K];
-  R sc[K];
+  constexpr double MU = double(SNUM) / double(SDEN);  // constant factor of every output (lift layers)
+  constexpr int NG = C::TG != 32 ? 1 : (8 * CNT <= 32) ? 8 : (4 * CNT <= 32) ? 4 : (2 * CNT <= 32) ? 2 : 1;  // (-3 % at TG=64)
+  constexpr int GF = 8 / NG;  // arrays per lane
+  if constexpr (NG == 1) {
+    constexpr int K = (CNT + C::TG - 1) / C::TG;
+    ushort4 o[K];
+    R sc[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int ic = cmin(q + C::TG * k, CNT - 1);
-    o[k] = __ldg(tab + ic);
-    sc[k] = SCALED ? __ldg(scale + ic) : R(1);
-  }
+    for (int k = 0; k < K; ++k) {
+      const int ic = cmin(q + C::TG * k, CNT - 1);
+      o[k] = __ldg(tab + ic);
+      sc[k] = SCALED ? __ldg(scale + ic) : R(1);
+    }
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int i = q + C::TG * k;
-    if (!((CNT % C::TG == 0) || i < CNT)) continue;
-    const char* p0 = gb + o[k].x + SRC * C::RB;
-    const char* p1 = gb + o[k].y + SRC * C::RB;
-    const char* p2 = gb + o[k].z + SRC * C::RB;
+    for (int k = 0; k < K; ++k) {
+      const int i = q + C::TG * k;
+      if (!((CNT % C::TG == 0) || i < CNT)) continue;
+      const char* p0 = gb + o[k].x + SRC * C::RB;
+      const char* p1 = gb + o[k].y + SRC * C::RB;
+      const char* p2 = gb + o[k].z + SRC * C::RB;
 #pragma unroll
-    for (int ff = 0; ff < 8; ++ff)
+      for (int ff = 0; ff < 8; ++ff)
 #pragma unroll
-      for (int u = 0; u < C::ET; ++u) {
-        const int so = ff * SSTRIDE * C::RB + u * C::EB;
-        R v = ld<R>(p0 + so) + ld<R>(p1 + so) + ld<R>(p2 + so);
-        if constexpr (SCALED) v *= sc[k];
-        st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, v);
-      }
+        for (int u = 0; u < C::ET; ++u) {
+          const int so = ff * SSTRIDE * C::RB + u * C::EB;
+          R v = ld<R>(p0 + so) + ld<R>(p1 + so) + ld<R>(p2 + so);
+          if constexpr (SCALED) v *= sc[k];
+          if constexpr (SNUM != SDEN) v *= R(MU);
+          st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, v);
+        }
+    }
+  } else {
+    if (q < NG * CNT) {
+      const int g = q / CNT, i = q - g * CNT;
+      const ushort4 o = __ldg(tab + i);
+      const R sc = SCALED ? __ldg(scale + i) : R(1);
+      const int fo = g * GF * SSTRIDE * C::RB;
+      const char* p0 = gb + o.x + SRC * C::RB + fo;
+      const char* p1 = gb + o.y + SRC * C::RB + fo;
+      const char* p2 = gb + o.z + SRC * C::RB + fo;
+      char* d = gb + (DST + g * GF * DSTRIDE + i) * C::RB;
+#pragma unroll
+      for (int ff = 0; ff < GF; ++ff)
+#pragma unroll
+        for (int u = 0; u < C::ET; ++u) {
+          const int so = ff * SSTRIDE * C::RB + u * C::EB;
+          R v = ld<R>(p0 + so) + ld<R>(p1 + so) + ld<R>(p2 + so);
+          if constexpr (SCALED) v *= sc;
+          if constexpr (SNUM != SDEN) v *= R(MU);
+          st<R>(d + ff * DSTRIDE * C::RB + u * C::EB, v);
+        }
+    }
   }
 }
 
@@ -411,9 +457,25 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
               R cv[LB];
 #pragma unroll
               for (int b1 = 0; b1 < LB; ++b1) cv[b1] = ld<R>(gb + (C::O_C + CB + b1) * RB + u * EB);
-              // only the vectors below the warp's la_max are loaded (predicated; x keeps stale values
-              // above it, which the FMAs below never read)
+              // only the vectors below the warp's la_max are loaded and only the a1 < la_max FMAs run:
+              // warp-uniform jumps into fall-through sequences (x keeps stale values above la_max,
+              // which are never read; the loads are opaque asm so x stays in registers)
               const unsigned pa = (unsigned)__cvta_generic_to_shared(pr + u * EB);
+#if BBW_PROD_SWITCH
+              auto ldv = [&](auto vc) {
+                constexpr int a1 = decltype(vc)::value * VEC;
+                if constexpr (a1 <= N) ld_shared_vec<R, a1 * C::RB>(&x[a1], pa);
+              };
+              BBW_FALLTHROUGH_SWITCH((lamax + VEC - 1) / VEC, ldv);
+              auto fm = [&](auto a1c) {
+                constexpr int a1 = decltype(a1c)::value;
+                if constexpr (a1 <= N) {
+#pragma unroll
+                  for (int b1 = 0; b1 < LB; ++b1) acc[u][a1 + b1] = fma(cv[b1], x[a1], acc[u][a1 + b1]);
+                }
+              };
+              BBW_FALLTHROUGH_SWITCH(lamax, fm);
+#else
               static_for<0, N + 1, VEC>([&](auto a1c) {
                 constexpr int a1 = decltype(a1c)::value;
                 ld_shared_vec_pred<R, a1 * C::RB>(&x[a1], pa, a1 < lamax);
@@ -425,6 +487,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
                   for (int b1 = 0; b1 < LB; ++b1) acc[u][a1 + b1] = fma(cv[b1], x[a1], acc[u][a1 + b1]);
                 }
               });
+#endif
             }
           }
         });
@@ -565,11 +628,8 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
   constexpr int N = C::N, M = C::M, NP = C::NP, NFP = C::NFP, NFP1 = C::NFP1, MP = C::MP, NPM1 = C::NPM1;
   constexpr int ET = C::ET, EB = C::EB, RB = C::RB, TG = C::TG, VEC = C::VEC, KO = C::KO;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ R lam_s[10];
   const int tid = threadIdx.x;
   const int grp = tid / TG, q = tid - grp * TG;
-  if (tid < 10) lam_s[tid] = A.lam[tid < 9 ? tid : 9];
-  __syncthreads();
   char* gb = reinterpret_cast<char*>(smem_raw) + grp * C::GB;  // this group's elements
   const GroupSync<C> sync{1 + grp};
   constexpr TabLayout L = tab_layout(N, M, RB);
@@ -937,7 +997,8 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
         constexpr int j = decltype(jc)::value;
         constexpr int m = N - j;
         if constexpr (j == 1) zero_region<C>(gb, q, C::Y_RPP, C::NS);  // padded r'' rows (F', Y'' are dead)
-        face_sum3<C, R, cnp2(m), C::X_L + layer_off(N, j - 1), NP, C::X_L + layer_off(N, j), NP, false>(
+        // layers are stored pre-multiplied by lam_j = (-1)^j/(j+1): s_j = -j/(j+1) R(s_{j-1}), s_0 = w'_0
+        face_sum3<C, R, cnp2(m), C::X_L + layer_off(N, j - 1), NP, C::X_L + layer_off(N, j), NP, false, -j, j + 1>(
             gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(m), static_cast<const R*>(nullptr));
         sync();
         BBW_PT(4);
@@ -953,16 +1014,14 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
           for (int f = 0; f < 4; ++f)
 #pragma unroll
             for (int dd = 0; dd < 3; ++dd) nrm[u][3 * f + dd] = ld<R>(gb + u * EB + (C::O_GEO + 12 + 4 * f + dd) * RB);
-        const uint4* lgt = reinterpret_cast<const uint4*>(tab + L.lg);
+        const uint2* lgt = reinterpret_cast<const uint2*>(tab + L.lg);
 #pragma unroll
         for (int k = 0; k < KO; ++k) {
           const int a = q + TG * k;
           if (a < NP) {
-            const uint4 e = __ldg(lgt + a);
+            const uint2 e = __ldg(lgt + a);
             const int lo[4] = {(int)(e.x & 0xFFFF), (int)(e.x >> 16), (int)(e.y & 0xFFFF), (int)(e.y >> 16)};
-            R lm[4];
-#pragma unroll
-            for (int f = 0; f < 4; ++f) lm[f] = lam_s[(e.z >> (8 * f)) & 0xFF];
+
             const R i1 = __ldg(invfacN + a), i2 = i1 * i1, f1 = __ldg(facN + a);  // 1/a!, 1/(a!)^2, a!
             const int pado = __ldg(padoff + a);
 #pragma unroll
@@ -971,8 +1030,8 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
               R sp = R(0), sx = R(0), sy = R(0), sz = R(0);
 #pragma unroll
               for (int f = 0; f < 4; ++f) {
-                const R wp = lm[f] * ld<R>(eb + (C::X_L + (2 * f) * NP) * RB + lo[f]);
-                const R wu = lm[f] * ld<R>(eb + (C::X_L + (2 * f + 1) * NP) * RB + lo[f]);
+                const R wp = ld<R>(eb + (C::X_L + (2 * f) * NP) * RB + lo[f]);  // lam_{a_f} already applied (D)
+                const R wu = ld<R>(eb + (C::X_L + (2 * f + 1) * NP) * RB + lo[f]);
                 sp += wp;
                 sx = fma(nrm[u][3 * f], wu, sx);
                 sy = fma(nrm[u][3 * f + 1], wu, sy);

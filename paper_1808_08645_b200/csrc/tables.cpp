@@ -271,8 +271,7 @@ HostTables build_tables(int N, int M, int RB) {
         for (int s = 0; s < 3; ++s) c[s] = a[FACE_V[f][s]];
         int li = (layer_off(N, j) + rank2(N - j, c[1], c[2])) * RB;
         if (li > 0xFFFF) throw std::runtime_error("lift offset overflow");
-        W.put<uint16_t>(L.lg + 16 * (int)i, f, (uint16_t)li);
-        W.put<uint8_t>(L.lg + 16 * (int)i + 8, f, (uint8_t)j);
+        W.put<uint16_t>(L.lg + 8 * (int)i, f, (uint16_t)li);
       }
     }
   }
