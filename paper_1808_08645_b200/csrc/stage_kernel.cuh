@@ -125,14 +125,15 @@ struct StageCfg {
   static constexpr int EB = PER_E * RB;  // element stride in bytes
   static constexpr int GB = ET * EB;     // group stride in bytes
   static constexpr int SMEM_BYTES = G * GB;
-  static_assert(TG % 32 == 0 && T % TG == 0 && G <= 15, "bad group shape");
+  static constexpr int GPW = TG < 32 ? 32 / TG : 1;  // groups per warp (sub-warp groups for small N)
+  static_assert((TG % 32 == 0 || 32 % TG == 0) && T % TG == 0 && (TG <= 32 || G <= 15), "bad group shape");
 };
 
 template <class C>
 struct GroupSync {
   int id;
   __device__ __forceinline__ void operator()() const {
-    if constexpr (C::TG == 32) {
+    if constexpr (C::TG <= 32) {  // sub-warp groups of one warp run the same phase sequence in lockstep
       __syncwarp();
     } else {
       asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(C::TG) : "memory");
@@ -646,12 +647,19 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
 
   const long long nelem = A.elem_end - A.elem_begin;
   const long long nbatch = (nelem + ET - 1) / ET;
-  for (long long batch = (long long)blockIdx.x * C::G + grp; batch < nbatch; batch += (long long)gridDim.x * C::G) {
+  // Sub-warp groups (TG < 32) share their warp's synchronisation, so the trip count is uniform per
+  // warp: the loop runs over the batch of the warp's first group, idle groups get nE = 0.
+  const int gw = grp % C::GPW;
+  for (long long bw = (long long)blockIdx.x * C::G + (grp - gw); bw < nbatch; bw += (long long)gridDim.x * C::G) {
+    const long long batch = bw + gw;
     const long long k0 = A.elem_begin + batch * ET;
     long long pt_prev = clock64();
     (void)pt_prev;
-    // valid elements of the batch (compile-time 1 for ET == 1: every batch start is < elem_end)
-    const int nE = (ET == 1) ? 1 : (int)((A.elem_end - k0) < ET ? (A.elem_end - k0) : ET);
+    // valid elements of the batch (compile-time 1 for ET == 1 and whole-warp groups: every batch
+    // start is < elem_end)
+    const int nE = (ET == 1 && C::GPW == 1)
+                       ? 1
+                       : (batch >= nbatch ? 0 : (int)((A.elem_end - k0) < ET ? (A.elem_end - k0) : ET));
 
     // ---- A: loads (Q, geometry, c'' -> smem via cp.async; the residual is only prefetched into L2
     //      here and read in phases D and J, so no registers are held across the WADG phases)

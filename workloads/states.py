@@ -42,30 +42,32 @@ def gaussian_pulse(vertices, elements, N: int, width: float = 50.0) -> np.ndarra
     return Q
 
 
-def manufactured_exact(x, y, z, t):
-    s = np.sin
-    c = np.cos
+def manufactured_exact(x, y, z, t, xp=np):
+    s = xp.sin
+    c = xp.cos
     pi = np.pi
-    p = s(pi * x) * s(pi * y) * s(pi * z) * c(pi * t)
-    ux = -c(pi * x) * s(pi * y) * s(pi * z) * s(pi * t)
-    uy = -s(pi * x) * c(pi * y) * s(pi * z) * s(pi * t)
-    uz = -s(pi * x) * s(pi * y) * c(pi * z) * s(pi * t)
+    st, ct = np.sin(pi * t), np.cos(pi * t)
+    p = s(pi * x) * s(pi * y) * s(pi * z) * ct
+    ux = -c(pi * x) * s(pi * y) * s(pi * z) * st
+    uy = -s(pi * x) * c(pi * y) * s(pi * z) * st
+    uz = -s(pi * x) * s(pi * y) * c(pi * z) * st
     return p, ux, uy, uz
 
 
-def manufactured_initial(vertices, elements, N: int, t: float = 0.0) -> np.ndarray:
+def manufactured_initial(vertices, elements, N: int, t: float = 0.0, device=None) -> np.ndarray:
     K = elements.shape[0]
     Q = np.zeros((K, 4, num_coeffs(N)))
     for c in range(4):
-        Q[:, c, :] = l2_fit(vertices, elements, lambda x, y, z, c=c: manufactured_exact(x, y, z, t)[c], N)
+        Q[:, c, :] = l2_fit(vertices, elements, lambda x, y, z, c=c, xp=np: manufactured_exact(x, y, z, t, xp)[c], N,
+                            device=device)
     return Q
 
 
-def manufactured_source(vertices, elements, N: int, c2func) -> np.ndarray:
+def manufactured_source(vertices, elements, N: int, c2func, device=None) -> np.ndarray:
     """g[K][Np] with r_p += g * sin(pi t)."""
     pi = np.pi
 
-    def f(x, y, z):
-        return (3.0 - 1.0 / c2func(x, y, z)) * pi * np.sin(pi * x) * np.sin(pi * y) * np.sin(pi * z)
+    def f(x, y, z, xp=np):
+        return (3.0 - 1.0 / c2func(x, y, z, xp=xp)) * pi * xp.sin(pi * x) * xp.sin(pi * y) * xp.sin(pi * z)
 
-    return l2_fit(vertices, elements, f, N)
+    return l2_fit(vertices, elements, f, N, device=device)
