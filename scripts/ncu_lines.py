@@ -41,6 +41,7 @@ _HELPERS = {}
 
 def helper_lines(src):
     """Lines of the tiny helpers (ld/st/static_for/cp_async) in the compiled copy of the source."""
+    src = os.environ.get("BBW_SRC") or src  # the copy the library was compiled from, if it moved on
     if src not in _HELPERS:
         out = set()
         try:
