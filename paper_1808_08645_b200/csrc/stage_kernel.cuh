@@ -65,8 +65,11 @@ struct StageArgs {
 #endif
 
 // default group shape per N: threads per group and elements per group-batch
-__host__ __device__ constexpr int default_tg(int N) { return N <= 7 ? 32 : 64; }
-__host__ __device__ constexpr int default_et(int N) { return N <= 2 ? 4 : N <= 4 ? 2 : 1; }
+// default group shape per N (A/B-measured, scripts/ab_subwarp*.sh): sub-warp groups of TG = 4 / 4 / 8 / 16
+// lanes per element for N = 1..4 (2.2x, 1.5x, 1.07x, 1.02x over whole-warp groups with 4 / 4 / 2 / 2
+// elements per lane), one warp per element for N = 5..7, two for N = 8, 9
+__host__ __device__ constexpr int default_tg(int N) { return N <= 2 ? 4 : N == 3 ? 8 : N == 4 ? 16 : N <= 7 ? 32 : 64; }
+__host__ __device__ constexpr int default_et(int N) { return N > 0 ? 1 : 1; }
 #ifndef BBW_MINB
 #define BBW_MINB 4
 #endif
@@ -190,8 +193,8 @@ __device__ __forceinline__ void cp_async_real(void* smem, const R* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-#ifndef BBW_PF
-#define BBW_PF 1
+#ifndef BBW_PF  // L2 prefetch of the next batch: no speed-up measured, +7 GB DRAM reads per config-5 stage
+#define BBW_PF 0
 #endif
 #ifndef BBW_LSRK_REG
 #define BBW_LSRK_REG 1
