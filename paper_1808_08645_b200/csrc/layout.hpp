@@ -21,7 +21,7 @@ __host__ __device__ constexpr int al16(int x) { return (x + 15) & ~15; }
 
 struct TabLayout {
   // byte offsets of the sections
-  int vg, ve, red, upw, lg, trired, triele, fnode, nbrvol, nbrface, csr_ptr, csr_terms, rowdec, padoff, rowlen;
+  int vg, ve, red, upw, lg, trired, triele, fnode, nbrvol, nbrface, rowdec, padoff, rowlen;
   int s_invfacN, s_facN, s_invfac2N, s_outN, s_invfacM, s_post, s_invfacNm1, s_cfac, s_invf2, s_cf2, s_rowpost;
   int total;
 };
@@ -36,7 +36,6 @@ struct TabLayout {
 // FNODE  [4][Np2(N)]        uint16: rank_N of face node i of face f, times RB
 // NBRVOL [24][Np2(N)]       uint16: rank_N of the matching neighbour node (code = 6 f' + sigma)
 // NBRFACE [6][Np2(N)]       uint16: neighbour face-local index (ghost traces)
-// CSR   ptr [Np(N+M)+1] int32, terms [Np(N) Np(M)] uint32 (alpha*RB | beta*RB << 16)
 // ROWDEC [Np2(N+M)]        uint32: rows (g2, g3) of degree N+M: g2 | g3 << 8 | rank_{N+M}(0,g2,g3) << 16
 // PADOFF [Np(N)]           uint16: byte offset of a in the zero-padded row copy (row stride RS)
 // ROWLEN [Np2(N)]          uint8: length N - a2 - a3 + 1 of row (a2, a3) of degree N
@@ -56,8 +55,6 @@ __host__ __device__ constexpr TabLayout tab_layout(int N, int M, int RB) {
   L.fnode = o;    o = al16(o + 2 * 4 * lnp2(N));
   L.nbrvol = o;   o = al16(o + 2 * 24 * lnp2(N));
   L.nbrface = o;  o = al16(o + 2 * 6 * lnp2(N));
-  L.csr_ptr = o;  o = al16(o + 4 * (lnp3(N + M) + 1));
-  L.csr_terms = o; o = al16(o + 4 * lnp3(N) * lnp3(M));
   L.rowdec = o;    o = al16(o + 4 * lnp2(N + M));
   L.padoff = o;    o = al16(o + 2 * lnp3(N));
   L.rowlen = o;    o = al16(o + lnp2(N));

@@ -357,8 +357,6 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   constexpr int N = C::N, M = C::M, NP = C::NP, NPH = C::NPH, RB = C::RB, ET = C::ET, EB = C::EB, TG = C::TG;
   constexpr TabLayout L = tab_layout(N, M, RB);
   const uint8_t* tab = A.tab;
-  const int* csr_ptr = reinterpret_cast<const int*>(tab + L.csr_ptr);
-  const uint32_t* csr = reinterpret_cast<const uint32_t*>(tab + L.csr_terms);
   const R* post = reinterpret_cast<const R*>(tab + L.s_post);
   const R* rowpost = reinterpret_cast<const R*>(tab + L.s_rowpost);
   const ushort4* red = reinterpret_cast<const ushort4*>(tab + L.red);
@@ -374,57 +372,6 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
     // whose input row does not exist read the zero row), and the unrolled a1 steps beyond the
     // warp's longest input row (la_max = N+1 - (min g2+g3 over the warp) + b2 + b3) are skipped by
     // warp-uniform branches, so the FMA count follows the real row lengths.
-#if BBW_PROD_V3  // round-1 v3 product (output rows in canonical order, divergent per c-row)
-#pragma unroll 1
-    for (int k = 0; k < KR; ++k) {
-      const int rho = q + TG * k;
-      if (rho < NR) {
-        const uint32_t d = __ldg(rowdec + rho);
-        const int g2 = d & 0xFF, g3 = (d >> 8) & 0xFF, gs = (int)(d >> 16);
-        R acc[ET][N + M + 1];
-#pragma unroll
-        for (int u = 0; u < ET; ++u)
-#pragma unroll
-          for (int x = 0; x <= N + M; ++x) acc[u][x] = R(0);
-        static_for<0, M + 1, 1>([&](auto b3c) {
-          constexpr int b3 = decltype(b3c)::value;
-          static_for<0, M + 1 - b3, 1>([&](auto b2c) {
-            constexpr int b2 = decltype(b2c)::value;
-            constexpr int LB = M - b2 - b3 + 1;
-            constexpr int CB = cnp3(M) - cnp3(M - b3) + b2 * (2 * (M - b3) + 3 - b2) / 2;  // rank_M(0,b2,b3)
-            const int a2 = g2 - b2, a3 = g3 - b3;
-            if (a2 >= 0 && a3 >= 0 && a2 + a3 <= N) {
-              const int m = N - a3;
-              const int la = m - a2 + 1;
-              const char* pr = gb + C::O_RP * RB + (cnp3(N) - (m + 1) * (m + 2) * (m + 3) / 6 + a2 * (2 * m + 3 - a2) / 2) * RB;
-#pragma unroll
-              for (int u = 0; u < ET; ++u) {
-                R in[N + 1];
-#pragma unroll
-                for (int a1 = 0; a1 <= N; ++a1)
-                  in[a1] = (a1 < la) ? ld<R>(pr + a1 * RB + u * EB) : R(0);
-#pragma unroll
-                for (int b1 = 0; b1 < LB; ++b1) {
-                  const R cv = ld<R>(gb + (C::O_C + CB + b1) * RB + u * EB);
-#pragma unroll
-                  for (int a1 = 0; a1 <= N; ++a1) acc[u][a1 + b1] = fma(cv, in[a1], acc[u][a1 + b1]);
-                }
-              }
-            }
-          });
-        });
-        const int lg = N + M - g2 - g3 + 1;
-#pragma unroll
-        for (int x = 0; x <= N + M; ++x) {
-          if (x < lg) {
-            const R s = __ldg(post + gs + x);
-#pragma unroll
-            for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + gs + x) * RB + u * EB, acc[u][x] * s);
-          }
-        }
-      }
-    }
-#else
     constexpr int VEC = C::VEC, RS = C::RS;
     R x[RS + VEC];
 #pragma unroll
@@ -526,7 +473,6 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         }
       }
     }
-#endif
   }
   sync();
   BBW_PT(6);

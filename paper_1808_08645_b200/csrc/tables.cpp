@@ -311,23 +311,6 @@ HostTables build_tables(int N, int M, int RB) {
         W.put<uint16_t>(L.nbrvol, (fp * 6 + sg) * NFP + i, (uint16_t)rank3(N, a[1], a[2], a[3]));
         if (fp == 0) W.put<uint16_t>(L.nbrface, sg * NFP + i, (uint16_t)rank2(N, d[1], d[2]));
       }
-  // CSR of the Bernstein product (Eq. mcoeff): for g in degree N+M, all (a, b) with a + b = g
-  {
-    auto iN = indices3(N), iM = indices3(M), iH = indices3(N + M);
-    int t = 0;
-    for (size_t gi = 0; gi < iH.size(); ++gi) {
-      W.put<int32_t>(L.csr_ptr, (int)gi, t);
-      const int* g = iH[gi].a;
-      for (size_t bi = 0; bi < iM.size(); ++bi) {
-        const int* b = iM[bi].a;
-        if (b[0] > g[0] || b[1] > g[1] || b[2] > g[2] || b[3] > g[3]) continue;
-        int ar = rank3(N, g[1] - b[1], g[2] - b[2], g[3] - b[3]);
-        W.put<uint32_t>(L.csr_terms, t++, (uint32_t)(ar * RB) | ((uint32_t)(bi * RB) << 16));
-      }
-    }
-    W.put<int32_t>(L.csr_ptr, (int)iH.size(), t);
-    if (t != lnp3(N) * lnp3(M)) throw std::runtime_error("CSR term count mismatch");
-  }
   // ROWDEC / ROWPOST: rows of degree N+M in warp passes of similar g2 + g3, lane order chosen
   // against shared-memory bank conflicts (product_row_order)
   {

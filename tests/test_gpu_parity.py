@@ -234,13 +234,13 @@ def test_nonfinite_detection(gpu_lib):
 
 
 # ------------------------------------------------------------------------------------ partitions
-@pytest.mark.parametrize("nparts", [2, 4, 8])
-def test_group_partition_bitwise(gpu_lib, nparts):
-    """P in-process partitions with device-copy halos == 1 partition, bitwise."""
+@pytest.mark.parametrize("nparts,N,M", [(2, 4, 2), (4, 4, 2), (8, 4, 2), (4, 7, 4), (8, 2, 1)])
+def test_group_partition_bitwise(gpu_lib, nparts, N, M):
+    """P in-process partitions with device-copy halos == 1 partition, bitwise; N = 2, 4 run
+    sub-warp element groups over the interior / boundary element ranges of each partition."""
     from paper_1808_08645_b200 import lib as L
 
     v, e = kuhn.kuhn_mesh(4)
-    N, M = 4, 2
     c2 = media.random_c2(len(e), M)
     Q0 = states.random_state(len(e), N)
     dt = 1e-3
@@ -287,7 +287,7 @@ def _neighbour_closure(e, sample):
     return np.unique(np.concatenate([sample, nb]))
 
 
-@pytest.mark.parametrize("cfg", ["config5", "config3_N9", "config4_f32"])
+@pytest.mark.parametrize("cfg", ["config5", "config3_N9", "config4_f32", "config3_N2", "config3_N4"])
 def test_full_size_sampled_parity(gpu_lib, cfg):
     """BASELINE.json configs at full size in the bench launch configuration: bbwadg_rhs on the
     whole mesh; the oracle recomputes 48 sampled elements (with their face neighbours)."""
@@ -297,6 +297,10 @@ def test_full_size_sampled_parity(gpu_lib, cfg):
         n, N, M, f, dtype, tol = 88, 7, 4, media.c2_smooth(1.0), "f64", 1e-12
     elif cfg == "config3_N9":
         n, N, M, f, dtype, tol = 44, 9, 9, media.c2_smooth(8.0), "f64", 1e-12
+    elif cfg == "config3_N2":  # sub-warp groups (4 lanes per element)
+        n, N, M, f, dtype, tol = 44, 2, 2, media.c2_smooth(8.0), "f64", 1e-12
+    elif cfg == "config3_N4":  # sub-warp groups (16 lanes per element)
+        n, N, M, f, dtype, tol = 44, 4, 4, media.c2_smooth(8.0), "f64", 1e-12
     else:
         n, N, M, f, dtype, tol = 56, 5, 3, media.c2_layered(), "f32", 1e-5
     v, e = kuhn.kuhn_mesh(n)
