@@ -353,7 +353,7 @@ __device__ __forceinline__ void zero_region(char* gb, int q, int off, int cnt) {
 
 template <class C, typename R>
 __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync,
-                                            long long& pt_prev) {
+                                            long long& pt_prev, R* osc) {
   constexpr int N = C::N, M = C::M, NP = C::NP, NPH = C::NPH, RB = C::RB, ET = C::ET, EB = C::EB, TG = C::TG;
   constexpr TabLayout L = tab_layout(N, M, RB);
   const uint8_t* tab = A.tab;
@@ -484,6 +484,12 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         st<R>(gb + C::W_A1 * RB + u * EB, R(0));
       }
     }
+  }
+  // the output scales a!/N! of phase J are requested here, off its critical path
+  {
+    const R* outN = reinterpret_cast<const R*>(tab + L.s_outN);
+#pragma unroll
+    for (int k = 0; k < C::KO; ++k) osc[k] = __ldg(outN + cmin(q + TG * k, NP - 1));
   }
   // G: M reductions N+M -> N (ping-pong H <-> P; the last lands in level N)
   static_for<N + M, N, -1>([&](auto nc) {
@@ -1023,7 +1029,8 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
     }
 
     // ---- F-I: WADG multiply + telescoping projection of r_p
-    wadg_phases<C, R>(gb, q, A, sync, pt_prev);
+    R osc[KO];
+    wadg_phases<C, R>(gb, q, A, sync, pt_prev, osc);
     constexpr int RES = wadg_result<C>();
 
     // ---- J: dp/dt = a!/N! b_N; outputs
@@ -1051,7 +1058,7 @@ __global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R
     for (int k = 0; k < KO; ++k) {
       const int a = q + TG * k;
       if (a < NP) {
-        const R sc = __ldg(outN + a);
+        const R sc = osc[k];
 #pragma unroll
         for (int u = 0; u < ET; ++u) {
           if (u >= nE) continue;
