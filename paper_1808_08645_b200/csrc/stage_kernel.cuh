@@ -70,9 +70,9 @@ struct StageArgs {
 // elements per lane), one warp per element for N = 5..7, two for N = 8, 9
 __host__ __device__ constexpr int default_tg(int N) { return N <= 2 ? 4 : N == 3 ? 8 : N == 4 ? 16 : N <= 7 ? 32 : 64; }
 __host__ __device__ constexpr int default_et(int N) { return N > 0 ? 1 : 1; }
-#ifndef BBW_MINB
-#define BBW_MINB 4
-#endif
+// minimum resident CTAs per SM for __launch_bounds__ (caps registers at 65536 / (T * MINB)); A/B-measured
+// (scripts/ab_minb.sh): 5 for N = 4, 5 (+3.6 %, +2..3 %), 4 elsewhere (N=6: -5.7 %, N=7: -15 % at 5)
+__host__ __device__ constexpr int default_minb(int N) { return (N == 4 || N == 5) ? 5 : 4; }
 
 template <int N_, int M_, typename R>
 struct StageCfg {
@@ -91,6 +91,11 @@ struct StageCfg {
   static constexpr int ET = BBW_ET;
 #else
   static constexpr int ET = default_et(N);
+#endif
+#ifdef BBW_MINB
+  static constexpr int MINB = BBW_MINB;
+#else
+  static constexpr int MINB = default_minb(N);
 #endif
   static constexpr int G = T / TG;               // groups per CTA
   static constexpr int KO = (NP + TG - 1) / TG;  // owned coefficients per thread
@@ -580,7 +585,7 @@ __host__ __device__ constexpr int wadg_result() {
 }
 
 template <class C, typename R>
-__global__ void __launch_bounds__(C::T, BBW_MINB) stage_kernel(const StageArgs<R> A) {
+__global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R> A) {
   constexpr int N = C::N, M = C::M, NP = C::NP, NFP = C::NFP, NFP1 = C::NFP1, MP = C::MP, NPM1 = C::NPM1;
   constexpr int ET = C::ET, EB = C::EB, RB = C::RB, TG = C::TG, VEC = C::VEC, KO = C::KO;
   extern __shared__ __align__(16) unsigned char smem_raw[];
