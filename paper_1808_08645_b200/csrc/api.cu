@@ -800,6 +800,6 @@ int bbwadg_debug_phase_times(bbwadg_ctx c, unsigned long long* out) {
   return 0;
 }
 
-const char* bbwadg_version(void) { return "bbwadg-b200 0.1 (sm_100a, fused stage kernel v1)"; }
+const char* bbwadg_version(void) { return "bbwadg-b200 0.1 (sm_100a, fused stage kernel v4)"; }
 
 }  // extern "C"
