@@ -245,6 +245,20 @@ __device__ __forceinline__ void ld_shared_vec(R* x, unsigned addr) {
 #define BBW_PROD_SWITCH 0  // measured 4-6 % slower than the predicated loads + branches
 #endif
 
+// LSRK outputs (Q_out, residual): streaming stores (evict-first), so the L2 keeps the stage input
+// Q_in that neighbour face traces are read from
+#ifndef BBW_STCS
+#define BBW_STCS 0  // measured: no DRAM saving, -0.6 % at N=7
+#endif
+template <typename R>
+__device__ __forceinline__ void st_out(R* p, R v) {
+#if BBW_STCS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 template <typename R>
 __device__ __forceinline__ R ld(const char* p) { return *reinterpret_cast<const R*>(p); }
 template <typename R>
@@ -1018,8 +1032,8 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
                   const long long gi = kk * 4 * NP + (1 + d) * NP + a;
                   if (A.mode == 0) {
                     const R r = fma(A.rk_a, BBW_SU(u, d, k), A.dt * r3[d]);
-                    A.res[gi] = r;
-                    A.Qout[gi] = fma(A.rk_b, r, BBW_QU(u, d, k));
+                    st_out(A.res + gi, r);
+                    st_out(A.Qout + gi, fma(A.rk_b, r, BBW_QU(u, d, k)));
                   } else {
                     A.Qout[gi] = r3[d];
                   }
@@ -1075,8 +1089,8 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
             const long long gi = kk * 4 * NP + a;
             if (A.mode == 0) {
               const R r = fma(A.rk_a, BBW_SP(u, k), A.dt * dp);
-              A.res[gi] = r;
-              A.Qout[gi] = fma(A.rk_b, r, BBW_QP(u, k));
+              st_out(A.res + gi, r);
+              st_out(A.Qout + gi, fma(A.rk_b, r, BBW_QP(u, k)));
             } else {
               A.Qout[gi] = dp;
             }
