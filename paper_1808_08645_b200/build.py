@@ -21,6 +21,9 @@ CSRC = os.path.join(HERE, "csrc")
 # BBWADG_VARIANT=<name> + BBWADG_DEFS="-DBBW_T=128 ..." build a tuning variant into native/<name>/
 VARIANT = os.environ.get("BBWADG_VARIANT", "")
 EXTRA_DEFS = os.environ.get("BBWADG_DEFS", "").split()
+if EXTRA_DEFS and not VARIANT:
+    # tuning defines must not leak into (or hide inside) the production library
+    raise SystemExit("BBWADG_DEFS needs BBWADG_VARIANT=<name> (builds into native/<name>/)")
 BUILD = os.path.join(HERE, "build", VARIANT) if VARIANT else os.path.join(HERE, "build")
 LIBDIR = os.path.join(HERE, "native", VARIANT) if VARIANT else os.path.join(HERE, "native")
 LIB = os.path.join(LIBDIR, "libbbwadg.so")
@@ -40,9 +43,21 @@ def _headers_mtime():
     return max(os.path.getmtime(h) for h in hs)
 
 
-def _compile(src: str, hdr_mtime: float, verbose: bool) -> str:
+def _defs_stamp_changed() -> bool:
+    """A variant rebuilt with different BBWADG_DEFS must recompile every object."""
+    stamp = os.path.join(BUILD, "defs.txt")
+    want = " ".join(EXTRA_DEFS)
+    have = open(stamp).read() if os.path.exists(stamp) else None
+    if have != want:
+        with open(stamp, "w") as fh:
+            fh.write(want)
+        return True
+    return False
+
+
+def _compile(src: str, hdr_mtime: float, verbose: bool, force: bool = False) -> str:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
+    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj
     cmd = [NVCC, *ARCH, *FLAGS, *EXTRA_DEFS, "-c", src, "-o", obj]
     if src.endswith(".cpp"):
@@ -65,9 +80,10 @@ def build(jobs: int | None = None, clean: bool = False, verbose: bool = False) -
     os.makedirs(LIBDIR, exist_ok=True)
     hm = _headers_mtime()
     srcs = _sources()
+    force = _defs_stamp_changed()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        objs = list(ex.map(lambda s: _compile(s, hm, verbose), srcs))
+        objs = list(ex.map(lambda s: _compile(s, hm, verbose, force), srcs))
     if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     tmp = LIB + ".tmp"

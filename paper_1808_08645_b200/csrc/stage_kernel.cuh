@@ -241,6 +241,22 @@ __device__ __forceinline__ void ld_shared_vec(R* x, unsigned addr) {
   }
 }
 
+// smallest g2 + g3 among the product output rows of a pass starting at ROWDEC entry r0: ROWDEC is sorted
+// by s = g2 + g3 and only permuted inside 32-row blocks (tables.cpp), so it is the s of row 32*floor(r0/32)
+__host__ __device__ constexpr int prod_pass_smin(int r0) {
+  int b = r0 / 32 * 32, s = 0;
+  while ((s + 1) * (s + 2) / 2 <= b) ++s;
+  return s;
+}
+__host__ __device__ constexpr int prod_acc_off(int nm, int tg, int k) {
+  int o = 0;
+  for (int j = 0; j < k; ++j) o += nm + 1 - prod_pass_smin(tg * j);
+  return o;
+}
+__host__ __device__ constexpr int prod_acc_total(int nm, int tg, int kr) { return prod_acc_off(nm, tg, kr); }
+#ifndef BBW_PROD_V5
+#define BBW_PROD_V5 1
+#endif
 #ifndef BBW_PROD_SWITCH
 #define BBW_PROD_SWITCH 0  // measured 4-6 % slower than the predicated loads + branches
 #endif
@@ -380,6 +396,127 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   const R* rowpost = reinterpret_cast<const R*>(tab + L.s_rowpost);
   const ushort4* red = reinterpret_cast<const ushort4*>(tab + L.red);
 
+#if BBW_PROD_V5
+  // F (v5): h'_g = post_g * sum_{a+b=g} r''_a c''_b (Eq. mcoeff), output-row stationary with
+  // the c''-row loop OUTSIDE the warp passes: every c''-row (b2,b3) is loaded once per element (not once
+  // per pass), and each lane loads only the vectors of ITS input row (g2-b2, g3-b3) that exist
+  // (predicated on the lane's own row length, not on the warp's longest row), so shared-memory bytes
+  // follow the real rows; the FMAs of a vector run under the same predicate.  All passes' row
+  // accumulators are live at once; pass k only holds rows with g2+g3 >= SMIN(k) (ROWDEC is sorted by
+  // g2+g3 and permuted only within 32-row blocks), which bounds its compile-time row length.
+  {
+    constexpr int NR = cnp2(N + M), KR = (NR + TG - 1) / TG;
+    constexpr int VEC = C::VEC, RS = C::RS, LH = N + M + 1;
+    const uint32_t* rowdec = reinterpret_cast<const uint32_t*>(tab + L.rowdec);
+    int g2v[KR], g3v[KR], gsv[KR], rid0v[KR];
+    bool actv[KR];
+    R rowfv[KR];
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      const int rho = q + TG * k;
+      actv[k] = rho < NR;
+      const uint32_t d = __ldg(rowdec + (actv[k] ? rho : NR - 1));
+      rowfv[k] = __ldg(rowpost + (actv[k] ? rho : NR - 1));
+      g2v[k] = d & 0xFF;
+      g3v[k] = (d >> 8) & 0xFF;
+      gsv[k] = (int)(d >> 16);
+      rid0v[k] = g3v[k] * (2 * N + 3 - g3v[k]) / 2 + g2v[k];
+    }
+    // flat accumulator: pass k owns entries [AOFF(k), AOFF(k) + LH - SMIN(k)) (compile-time sizes)
+    constexpr int ATOT = prod_acc_total(N + M, TG, KR);
+    R acc[ET][ATOT];
+#pragma unroll
+    for (int u = 0; u < ET; ++u)
+#pragma unroll
+      for (int x = 0; x < ATOT; ++x) acc[u][x] = R(0);
+    static_for<0, M + 1, 1>([&](auto b3c) {
+      constexpr int b3 = decltype(b3c)::value;
+      static_for<0, M + 1 - b3, 1>([&](auto b2c) {
+        constexpr int b2 = decltype(b2c)::value;
+        constexpr int LB = M - b2 - b3 + 1;
+        constexpr int CB = cnp3(M) - cnp3(M - b3) + b2 * (2 * (M - b3) + 3 - b2) / 2;  // rank_M(0,b2,b3)
+        R cv[ET][LB];
+#pragma unroll
+        for (int u = 0; u < ET; ++u)
+#pragma unroll
+          for (int b1 = 0; b1 < LB; ++b1) cv[u][b1] = ld<R>(gb + (C::O_C + CB + b1) * RB + u * EB);
+        static_for<0, KR, 1>([&](auto kc) {
+          constexpr int k = decltype(kc)::value;
+          constexpr int SMIN = prod_pass_smin(TG * k);
+          constexpr int LA = cmin(N + 1, N + 1 - SMIN + b2 + b3);  // longest input row pass k can meet
+          if constexpr (LA > 0) {
+            const int a2 = g2v[k] - b2, a3 = g3v[k] - b3;
+            const bool valid = actv[k] && a2 >= 0 && a3 >= 0 && a2 + a3 <= N;
+            const int lenA = valid ? N + 1 - a2 - a3 : 0;
+            const int lamax = __reduce_max_sync(0xffffffffu, lenA);
+            if (lamax > 0) {
+              const int rid = rid0v[k] + b3 * g3v[k] - b3 * (2 * N + 3 + b3) / 2 - b2;  // rowid(a2, a3)
+              const char* pr = gb + (C::Y_RPP + (valid ? rid : 0) * RS) * RB;
+#pragma unroll
+              for (int u = 0; u < ET; ++u) {
+                const unsigned pa = (unsigned)__cvta_generic_to_shared(pr + u * EB);
+                static_for<0, LA, VEC>([&](auto vc) {
+                  constexpr int v0 = decltype(vc)::value;
+                  if (v0 < lamax) {  // warp-uniform
+                    const bool pv = v0 < lenA;
+                    R x[VEC];
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) x[i] = R(0);
+                    ld_shared_vec_pred<R, v0 * C::RB>(x, pa, pv);
+#pragma unroll
+                    for (int i = 0; i < VEC; ++i) {
+                      if (v0 + i < LA) {
+#pragma unroll
+                        for (int b1 = 0; b1 < LB; ++b1) {
+                          constexpr int AO = prod_acc_off(N + M, TG, k);
+                          acc[u][AO + v0 + i + b1] = fma(cv[u][b1], x[i], acc[u][AO + v0 + i + b1]);
+                        }
+                      }
+                    }
+                  }
+                });
+              }
+            }
+          }
+        });
+      });
+    });
+    // outputs: h'_g = N!M!/(N+M)! (g!)^2 h''_g, g = (lg-1-x, x, g2, g3), as v4 below
+    static_for<0, KR, 1>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      constexpr int LMAX = LH - prod_pass_smin(TG * k);
+      constexpr int AO = prod_acc_off(N + M, TG, k);
+      if (actv[k]) {
+        const int lg = N + M - g2v[k] - g3v[k] + 1;
+        if constexpr (N + M <= 12) {
+          R P = rowfv[k], T = R(lg - (N + M));
+          static_for<N + M, -1, -1>([&](auto xc) {
+            constexpr int x = decltype(xc)::value;
+            if constexpr (x < LMAX) {
+              if (x < lg) {
+#pragma unroll
+                for (int u = 0; u < ET; ++u)
+                  st<R>(gb + (C::W_H + gsv[k] + x) * RB + u * EB, acc[u][AO + x] * (R(fact2c(x)) * P));
+              }
+            }
+            const R Tc = T > R(1) ? T : R(1);
+            P *= Tc * Tc;
+            T += R(1);
+          });
+        } else {
+#pragma unroll
+          for (int x = 0; x < LMAX; ++x) {
+            if (x < lg) {
+              const R sp = __ldg(post + gsv[k] + x);
+#pragma unroll
+              for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + gsv[k] + x) * RB + u * EB, acc[u][AO + x] * sp);
+            }
+          }
+        }
+      }
+    });
+  }
+#else
   // F: h'_g = post_g * sum_{a+b=g} r''_a c''_b, output-row stationary: for output row (g2,g3) of
   // degree N+M and every c''-row (b2,b3), the input row (g2-b2, g3-b3) of r'' is loaded once into
   // registers and convolved (1-D, full) with the c''-row into the row accumulators.
@@ -493,6 +630,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
       }
     }
   }
+#endif
   sync();
   BBW_PT(6);
   if constexpr (!C::ALIAS) {

@@ -326,3 +326,143 @@ def test_manufactured_convergence_rate():
         errs.append(o.l2_error(Q, states.manufactured_exact, T))
     rate = np.log2(errs[0] / errs[1])
     assert rate > 2.7, (errs, rate)
+
+
+# --------------------------------------------------------------------------- penalty scale (Eq. sdf)
+def _face_energy_loss(v, e, N, Q, tau_p, tau_u):
+    """-dE/dt predicted from the face jumps alone (Eq. sdf; derivation in DESIGN.md §3):
+    summing p r_p + u.r_u over the two sides of an interior face, the central parts cancel and
+    -int_f (tau_p/2 [[p]]^2 + tau_u/2 [[u.n]]^2) remains; on a pressure-release boundary face
+    (p+ = -p, u+ = u, R11) the sum is -tau_p int_f p^2.  Computed here from physical face points,
+    the test's own affine maps and normals (no oracle operator is used)."""
+    X = v[e]  # K,4,3
+    K = len(e)
+    keys = {}
+    for k in range(K):
+        for f in range(4):
+            keys.setdefault(tuple(sorted(int(x) for j, x in enumerate(e[k]) if j != f)), []).append((k, f))
+    lam3, w = qd.tri_rule(N + 1)  # exact to degree 2N+1 on the face
+    lam3 = lam3.astype(np.float64)
+    w = w.astype(np.float64)
+
+    def evaluate(k, x):  # fields of element k at physical points x[nq,3]
+        E = np.stack([X[k, 1] - X[k, 0], X[k, 2] - X[k, 0], X[k, 3] - X[k, 0]], axis=1)
+        l = np.linalg.solve(E, (x - X[k, 0]).T).T
+        lam = np.concatenate([1 - l.sum(1, keepdims=True), l], axis=1)
+        return np.einsum("qi,ci->cq", bb.eval_basis(N, lam), Q[k])
+
+    loss = 0.0
+    for pairs in keys.values():
+        k, f = pairs[0]
+        others = [j for j in range(4) if j != f]
+        P3 = X[k, others]
+        x = lam3 @ P3
+        cr = np.cross(P3[1] - P3[0], P3[2] - P3[0])
+        area = 0.5 * np.linalg.norm(cr)
+        n = cr / np.linalg.norm(cr)
+        if np.dot(n, P3[0] - X[k, f]) < 0:
+            n = -n
+        qm = evaluate(k, x)
+        if len(pairs) == 1:
+            loss += tau_p * area * np.sum(w * qm[0] ** 2)
+        else:
+            qp = evaluate(pairs[1][0], x)
+            jp = qp[0] - qm[0]
+            jun = n @ (qp[1:4] - qm[1:4])
+            loss += area * np.sum(w * (0.5 * tau_p * jp ** 2 + 0.5 * tau_u * jun ** 2))
+    return loss
+
+
+@pytest.mark.parametrize("tau", [(1.0, 1.0), (0.5, 2.0), (0.0, 3.0)])
+def test_energy_rate_equals_penalty_face_integrals(tau):
+    # pins the penalty SCALE of Eq. sdf (P:98-107), not only its sign: dE/dt = -sum of the face
+    # integrals of tau_p/2 [[p]]^2 + tau_u/2 [[u.n]]^2 (interior) and tau_p p^2 (boundary)
+    N, M = 3, 1
+    v, e = kuhn.kuhn_mesh(2)
+    o = AcousticOracle(v, e, N, M, media.random_c2(len(e), M), tau_p=tau[0], tau_u=tau[1])
+    for s in range(2):
+        Q = np.random.default_rng(100 + s).standard_normal((len(e), 4, bb.num_coeffs(N)))
+        pred = -_face_energy_loss(v, e, N, Q, *tau)
+        assert abs(o.energy_rate(Q) - pred) <= 1e-12 * abs(pred), (o.energy_rate(Q), pred)
+
+
+def test_energy_rate_pin_detects_penalty_mutation():
+    # mutation check of the pin above: an oracle whose penalty is doubled (the "dropped 1/2" class
+    # of mistakes on tau) must fail it
+    N, M = 2, 1
+    v, e = kuhn.kuhn_mesh(2)
+    c2 = media.random_c2(len(e), M)
+    Q = np.random.default_rng(7).standard_normal((len(e), 4, bb.num_coeffs(N)))
+    pred = -_face_energy_loss(v, e, N, Q, 1.0, 1.0)
+    for tp, tu in [(2.0, 1.0), (1.0, 2.0)]:
+        o = AcousticOracle(v, e, N, M, c2, tau_p=tp, tau_u=tu)
+        assert abs(o.energy_rate(Q) - pred) > 1e-3 * abs(pred)
+
+
+# --------------------------------------------------------------------------- LSRK stage times
+def _lsrk_scalar(A, B, C, f, t0, dt):
+    """One 2N-storage step of y' = f(t) (y-independent), exact rational arithmetic."""
+    y, res = Fraction(0), Fraction(0)
+    for s in range(5):
+        res = A[s] * res + dt * f(t0 + C[s] * dt)
+        y = y + B[s] * res
+    return y
+
+
+def test_lsrk_stage_times_are_the_implied_abscissae():
+    # c_s is the time the stage input represents: the stage-s value of y' = 1, y(0) = 0, dt = 1
+    # (P:1264 cites Carpenter-Kennedy; DESIGN.md R13)
+    from oracle.acoustic import LSRK_A, LSRK_B, LSRK_C
+    y, res = Fraction(0), Fraction(0)
+    for s in range(5):
+        assert abs(float(y - LSRK_C[s])) < 1e-11, (s, float(y), float(LSRK_C[s]))
+        res = LSRK_A[s] * res + 1
+        y = y + LSRK_B[s] * res
+    assert abs(float(y) - 1.0) < 1e-11
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_lsrk_integrates_polynomials_in_time(k):
+    # 4th order (P:1264): y' = k t^(k-1) is integrated exactly for k <= 4 -- this uses the stage
+    # times, which the stability polynomial cannot see
+    from oracle.acoustic import LSRK_A, LSRK_B, LSRK_C
+    y = _lsrk_scalar(LSRK_A, LSRK_B, LSRK_C, lambda t: k * t ** (k - 1), Fraction(0), Fraction(1))
+    assert abs(float(y) - 1.0) < 1e-11
+    # mutation check: c_3 * (1 + 1e-6) breaks it for k >= 2
+    if k >= 2:
+        C = list(LSRK_C)
+        C[3] = C[3] * (1 + Fraction(1, 10 ** 6))
+        y = _lsrk_scalar(LSRK_A, LSRK_B, C, lambda t: k * t ** (k - 1), Fraction(0), Fraction(1))
+        assert abs(float(y) - 1.0) > 1e-8
+
+
+def test_oracle_step_uses_stage_times():
+    # a time-dependent source makes the stage times visible: the oracle's step must equal the
+    # 2N-storage recursion evaluated at t0 + c_s dt with c_s the abscissae IMPLIED by (A, B)
+    # (computed here, not read from LSRK_C)
+    from oracle.acoustic import LSRK_A, LSRK_B
+    N, M = 2, 1
+    v, e = kuhn.kuhn_mesh(2)
+    c2 = media.random_c2(len(e), M)
+    g = np.random.default_rng(3).standard_normal((len(e), bb.num_coeffs(N)))
+    o = AcousticOracle(v, e, N, M, c2, source=g)
+    c, y, r = [], Fraction(0), Fraction(0)
+    for s in range(5):
+        c.append(float(y))
+        r = LSRK_A[s] * r + 1
+        y = y + LSRK_B[s] * r
+    t0, dt = 0.3, 0.05
+    Q0 = 1e-3 * np.random.default_rng(4).standard_normal((len(e), 4, bb.num_coeffs(N)))
+    Q = o.run(Q0, t0, dt, 1)
+    q, res = Q0.copy(), np.zeros_like(Q0)
+    for s in range(5):
+        res = float(LSRK_A[s]) * res + dt * o.rhs(q, t0 + c[s] * dt)
+        q = q + float(LSRK_B[s]) * res
+    assert np.max(np.abs(Q - q)) <= 1e-13 * np.max(np.abs(q))
+    # the source term is not negligible here: shifting c_3 by 1e-6 moves the result above that bar
+    res, q2 = np.zeros_like(Q0), Q0.copy()
+    for s in range(5):
+        cs = c[s] * (1 + 1e-6) if s == 3 else c[s]
+        res = float(LSRK_A[s]) * res + dt * o.rhs(q2, t0 + cs * dt)
+        q2 = q2 + float(LSRK_B[s]) * res
+    assert np.max(np.abs(q2 - q)) > 1e-12 * np.max(np.abs(q))
