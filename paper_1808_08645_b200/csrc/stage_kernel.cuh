@@ -132,7 +132,7 @@ struct StageCfg {
   static constexpr int PER_E = rup(O_X + cmax(XSIZE + YSIZE, WSIZE), VEC);
   static constexpr int EB = PER_E * RB;  // element stride in bytes
   static constexpr int GB = ET * EB;     // group stride in bytes
-  static constexpr int SMEM_BYTES = G * GB;
+  static constexpr int SMEM_BYTES = G * GB + 8 * G;  // + one mbarrier per group (TMA bulk loads)
   static constexpr int GPW = TG < 32 ? 32 / TG : 1;  // groups per warp (sub-warp groups for small N)
   static_assert((TG % 32 == 0 || 32 % TG == 0) && T % TG == 0 && (TG <= 32 || G <= 15), "bad group shape");
 };
@@ -195,6 +195,30 @@ __device__ __forceinline__ void cp_async_real(void* smem, const R* gmem) {
                "n"((int)sizeof(R))
                : "memory");
 }
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on a per-group mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(mbar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(mbar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}" ::"r"((unsigned)__cvta_generic_to_shared(mbar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
@@ -206,6 +230,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 #endif
 #ifndef BBW_CPASYNC
 #define BBW_CPASYNC 1
+#endif
+#ifndef BBW_TMA
+#define BBW_TMA 1  // element Q blocks, geometry and neighbour ids by cp.async.bulk (needs BBW_CPASYNC)
 #endif
 
 // predicated 16-B shared load into x[0..VEC): registers keep their old values when !p
@@ -759,6 +786,13 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
 
   const long long nelem = A.elem_end - A.elem_begin;
   const long long nbatch = (nelem + ET - 1) / ET;
+#if BBW_TMA && BBW_CPASYNC
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + C::G * C::GB) + grp;
+  unsigned mbar_phase = 0;
+  if (q == 0) mbar_init(mbar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+#endif
   // Sub-warp groups (TG < 32) share their warp's synchronisation, so the trip count is uniform per
   // warp: the loop runs over the batch of the warp's first group, idle groups get nE = 0.
   const int gw = grp % C::GPW;
@@ -811,6 +845,22 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
       constexpr int NV = 4 * NP / VEC;  // 16-B chunks of Q
       constexpr int GV = 12 * RB / 16;  // 16-B chunks of grad(lambda)
       const char* gq = reinterpret_cast<const char*>(A.Qin + k0 * 4 * NP);
+#if BBW_TMA
+      // one elected lane per group: Q block (4 Np reals), grad(lambda) (12 reals) and the 4 neighbour ids of
+      // every element of the batch by TMA bulk copies on the group's mbarrier (no LSU wavefronts)
+      (void)NV;
+      (void)gq;
+      if (q == 0 && nE > 0) {
+        mbar_expect_tx(mbar, (unsigned)nE * (4 * NP * RB + 12 * RB + 16));
+        for (int u = 0; u < nE; ++u) {
+          char* eb = gb + u * EB;
+          bulk_g2s(eb + C::X_Q * RB, A.Qin + (k0 + u) * 4 * NP, 4 * NP * RB, mbar);
+          bulk_g2s(eb + C::O_GEO * RB, A.geo + (k0 + u) * 12, 12 * RB, mbar);
+          bulk_g2s(eb + 28 * RB, A.nbr + (k0 + u) * 4, 16, mbar);
+        }
+      }
+      for (int u = q; u < nE; u += TG) cp_async4(gb + u * EB + 28 * RB + 16, A.code + (k0 + u) * 4);  // 4 codes
+#else
 #pragma unroll
       for (int t0 = 0; t0 < ET * NV; t0 += TG) {
         const int t = t0 + q;
@@ -826,6 +876,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         else if (w == GV) cp_async16(eb + 28 * RB, A.nbr + (k0 + u) * 4);     // 4 neighbour ids
         else cp_async4(eb + 28 * RB + 16, A.code + (k0 + u) * 4);             // 4 codes (bytes)
       }
+#endif
       for (int t = q; t < nE * MP; t += TG) {
         const int u = t / MP, b = t - u * MP;
         cp_async_real<R>(gb + u * EB + (C::O_C + b) * RB, A.c2 + (k0 + u) * MP + b);
@@ -847,6 +898,12 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
       }
 #endif
       cp_async_wait_all();
+#if BBW_TMA
+      if (nE > 0) {
+        mbar_wait(mbar, mbar_phase);
+        mbar_phase ^= 1;
+      }
+#endif
       sync();
       for (int t = q; t < nE * 4; t += TG) {  // outward normal, |grad lambda_f|
         const int u = t >> 2, f = t & 3;
@@ -1236,6 +1293,9 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         }
       }
     }
+#if BBW_TMA && BBW_CPASYNC
+    fence_proxy_async();  // this batch's generic smem accesses before the next batch's bulk (async-proxy) writes
+#endif
     sync();
     BBW_PT(10);
   }

@@ -70,7 +70,7 @@ class Solver:
             Q = np.ascontiguousarray(Q, dtype=self._host_dtype())
             L.bbwadg_set_state(self.ctx, Q, 0)
         else:
-            L.bbwadg_set_state(self.ctx, Q.contiguous(), 1)
+            L.bbwadg_set_state(self.ctx, self._check_dev(Q, (self.K_local, 4, self.Np), "Q"), 1)
 
     def get_state(self, device: bool = False):
         if device:
@@ -84,15 +84,29 @@ class Solver:
     def set_source(self, g):
         L.bbwadg_set_source(self.ctx, None if g is None else np.ascontiguousarray(g, dtype=np.float64))
 
+    def _check_dev(self, x, shape, what: str):
+        """Device tensors go to the C side as raw pointers: validate before they do."""
+        if not isinstance(x, self.torch.Tensor):
+            raise TypeError(f"{what} must be a torch tensor on {self.device}")
+        if x.device != self.device:
+            raise ValueError(f"{what} is on {x.device}, the solver on {self.device}")
+        if x.dtype != self.tdtype:
+            raise TypeError(f"{what} has dtype {x.dtype}, the solver computes in {self.tdtype}")
+        if tuple(x.shape) != shape:
+            raise ValueError(f"{what} has shape {tuple(x.shape)}, expected {shape}")
+        return x.contiguous()
+
     # -------------------------------------------------------------------------------- compute
     def rhs(self, Q_dev, t: float = 0.0):
-        out = self.torch.empty_like(Q_dev)
-        L.bbwadg_rhs(self.ctx, Q_dev.contiguous(), t, out)
+        Q_dev = self._check_dev(Q_dev, (self.K_local, 4, self.Np), "Q")
+        out = self.torch.empty(Q_dev.shape, dtype=self.tdtype, device=self.device)
+        L.bbwadg_rhs(self.ctx, Q_dev, t, out)
         return out
 
     def wadg_apply(self, r_dev):
-        out = self.torch.empty_like(r_dev)
-        L.bbwadg_wadg_apply(self.ctx, r_dev.contiguous(), out)
+        r_dev = self._check_dev(r_dev, (self.K_local, self.Np), "r")
+        out = self.torch.empty(r_dev.shape, dtype=self.tdtype, device=self.device)
+        L.bbwadg_wadg_apply(self.ctx, r_dev, out)
         return out
 
     def step(self, t: float, dt: float):
