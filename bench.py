@@ -39,7 +39,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "DOF-stage updates/sec per B200 (BBWADG acoustic RK stage, fused RHS + LSRK45)"
+METRIC = ("DOF-stage updates/sec, whole job over n_gpus B200s (value_per_gpu = per B200; BBWADG acoustic RK "
+          "stage, fused RHS + LSRK45)")
 UNIT = "DOF-stage/s"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 
@@ -64,6 +65,30 @@ def factor_cuts(p: int):
             if best is None or sc < best[0]:
                 best = (sc, (px, py, pz))
     return best[1]
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return os.uname().machine
+
+
+def pulse_state(v, e, N, device, width=50.0):
+    """SURVEY 8(d) bench state: p = exp(-width |x|^2), u = 0 (L2-projected on the device)."""
+    import torch
+
+    from workloads._l2fit import l2_fit
+
+    Np = comb(N + 3, 3)
+    Q = torch.zeros((e.shape[0], 4, Np), dtype=torch.float64, device=device)
+    p = l2_fit(v, e, lambda x, y, z, xp=np: xp.exp(-width * (x * x + y * y + z * z)), N, device=device)
+    Q[:, 0] = torch.from_numpy(p).to(device)
+    return Q
 
 
 def load_peaks():
@@ -168,10 +193,8 @@ def local_c2(v, e, cfunc, M, rank, world, cuts, device):
     if world == 1:
         return media.project_c2(v, e, cfunc, M, device=device), None
     plan = L.bbwadg_partition_plan(v, e, world, rank, cuts)
-    gid = plan["gid"]
-    c2 = np.ones((e.shape[0], Mp))
-    c2[gid] = media.project_c2(v, e[gid], cfunc, M, device=device)
-    return c2, gid
+    gid = np.ascontiguousarray(plan["gid"], dtype=np.int64)
+    return media.project_c2(v, e[gid], cfunc, M, device=device), gid  # local rows only (Solver c2_gids)
 
 
 def run_ours(args):
@@ -191,7 +214,7 @@ def run_ours(args):
     N, M = args.N, args.M
     Np = comb(N + 3, 3)
     v, e, cfunc, cuts, wname = build_workload(args, rank, world, device=dev)
-    c2, _ = local_c2(v, e, cfunc, M, rank, world, cuts, dev)
+    c2, c2_gids = local_c2(v, e, cfunc, M, rank, world, cuts, dev)
     nccl_id = None
     if world > 1:
         import torch.distributed as dist
@@ -201,7 +224,7 @@ def run_ours(args):
         nccl_id = idbuf[0]
     stream = torch.cuda.current_stream(dev)
     s = Solver(v, e, N, M, c2, dtype=args.dtype, device=local, stream=stream, rank=rank, world_size=world,
-               nccl_id=nccl_id, partition=cuts if world > 1 else None)
+               nccl_id=nccl_id, partition=cuts if world > 1 else None, c2_gids=c2_gids)
     info = s.info()
     K_local = info["num_elements_local"]
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -299,7 +322,8 @@ def run_ours(args):
                       "bbwadg_get_state(pinned host), host wall clock, max over ranks"}
         del hostQ
 
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    out = {"metric": METRIC, "value": value, "value_per_gpu": value / world, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
            "config": {"workload": wname, "N": N, "M": M, "K_total": K_total, "K_per_gpu": K_local,
@@ -312,6 +336,8 @@ def run_ours(args):
     s.close()
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(N, M, args.cpu_seconds, extras=True)
+    if rank == 0 and not args.no_config4:
+        out["config4"] = config4_runs(args, dev)
     if rank == 0 and not args.no_sweep:
         out["sweep"] = sweep(args, dev)
     if rank == 0:
@@ -321,6 +347,49 @@ def run_ours(args):
 
         dist.barrier()
         dist.destroy_process_group()
+
+
+def config4_runs(args, dev):
+    """BASELINE config 4: layered (discontinuous) c^2, n=56 Kuhn mesh (1,053,696 tets), N=5, M=3, fp64 and
+    fp32, Gaussian pulse state, 3 warm-up + 10 timed steps each, clocks sampled during the timed steps."""
+    import torch
+
+    from paper_1808_08645_b200 import Solver
+    from workloads import kuhn, media
+
+    n, N, M = 56, 5, 3
+    v, e = kuhn.kuhn_mesh(n)
+    c2 = media.project_c2(v, e, media.c2_layered(), M, device=dev)
+    Np = comb(N + 3, 3)
+    peaks, _ = load_peaks()
+    Q0 = pulse_state(v, e, N, dev)
+    out = {}
+    for dt_name in ("f64", "f32"):
+        s = Solver(v, e, N, M, c2, dtype=dt_name, device=dev.index, stream=torch.cuda.current_stream(dev))
+        s.set_state(Q0 if dt_name == "f64" else Q0.float())
+        h_min = 2.0 / n / (1 + np.sqrt(2) + np.sqrt(3))
+        dt = 0.5 * h_min / (np.sqrt(2.25) * (N + 1) ** 2)
+        for i in range(3):
+            s.step(i * dt, dt)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev.index) as clk:
+            torch.cuda.synchronize()
+            a.record()
+            for i in range(10):
+                s.step((3 + i) * dt, dt)
+            b.record()
+            torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        info = s.info()
+        gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
+        out[dt_name] = {"value": 4.0 * len(e) * Np * 5 / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                        "hbm_frac": gbs / peaks["hbm_gbs"], "achieved_gbs": gbs, "warmup": 3, "steps": 10,
+                        "clocks": clk.summary()}
+        s.close()
+    out["workload"] = (f"config4: Kuhn n={n} ({len(e):,} tets), N={N}, M={M}, layered c^2 1/1.5/2.25 (sub-cell "
+                       f"jumps), Gaussian pulse")
+    return out
 
 
 def sweep(args, dev):
@@ -339,19 +408,21 @@ def sweep(args, dev):
         Np = comb(N + 3, 3)
         c2 = media.project_c2(v, e, f, M, device=dev)
         s = Solver(v, e, N, M, c2, device=dev.index, stream=torch.cuda.current_stream(dev))
-        Q0 = torch.randn((len(e), 4, Np), dtype=torch.float64, device=dev)
-        s.set_state(Q0)
-        del Q0
-        for i in range(2):
-            s.step(0.0, 1e-4)
+        s.set_state(pulse_state(v, e, N, dev))
+        h_min = 2.0 / args.sweep_n / (1 + np.sqrt(2) + np.sqrt(3))
+        dt = 0.5 * h_min / (np.sqrt(1.5) * (N + 1) ** 2)
+        for i in range(args.sweep_warmup):
+            s.step(i * dt, dt)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        nst = 5
-        a.record()
-        for i in range(nst):
-            s.step(0.0, 1e-4)
-        b.record()
-        torch.cuda.synchronize()
+        nst = args.sweep_steps
+        with ClockSampler(dev.index) as clk:
+            torch.cuda.synchronize()
+            a.record()
+            for i in range(nst):
+                s.step((args.sweep_warmup + i) * dt, dt)
+            b.record()
+            torch.cuda.synchronize()
         ms = a.elapsed_time(b) / nst
         info = s.info()
         gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
@@ -359,12 +430,14 @@ def sweep(args, dev):
                      "ns_per_element_stage": ms * 1e6 / (5 * len(e)), "hbm_frac": gbs / peaks["hbm_gbs"],
                      "tflops": info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12,
                      "flops_per_element_stage": info["flops_per_stage"] / len(e),
-                     "bytes_per_element_stage": info["algorithmic_bytes_per_stage"] / len(e)})
+                     "bytes_per_element_stage": info["algorithmic_bytes_per_stage"] / len(e),
+                     "warmup": args.sweep_warmup, "steps": nst, "clocks": clk.summary()})
         s.close()
     sel = [r for r in rows if r["N"] >= 4]
     Ns = np.log(np.array([r["N"] for r in sel], dtype=float))
     fit = lambda y: float(np.polyfit(Ns, np.log(np.array(y, dtype=float)), 1)[0])
-    return {"workload": f"config3: Kuhn n={args.sweep_n} ({len(e):,} tets), M=N, c^2 k=8, fp64",
+    return {"workload": f"config3: Kuhn n={args.sweep_n} ({len(e):,} tets), M=N, c^2 k=8, Gaussian pulse "
+                        f"p = exp(-50|x|^2), u = 0, fp64; {args.sweep_warmup} warm-up + {args.sweep_steps} timed steps per N",
             "rows": rows, "loglog_slope_time_per_element_N4to9": fit([r["ns_per_element_stage"] for r in sel]),
             "loglog_slope_algorithmic_flops_N4to9": fit([r["flops_per_element_stage"] for r in sel]),
             "loglog_slope_algorithmic_bytes_N4to9": fit([r["bytes_per_element_stage"] for r in sel]),
@@ -400,7 +473,7 @@ def cpu_baseline(N, M, seconds, extras=False):
     out = {"value": 4.0 * len(e) * Np * 5 * steps / el, "unit": UNIT, "cores": cores, "kind": "oracle",
            "sample": f"{steps} LSRK45 step(s) of the oracle on a {len(e)}-tet Kuhn mesh (n={n}), N={N}, M={M}, "
                      f"fp64 numpy/BLAS; table setup {setup:.1f}s excluded",
-           "cpu": os.uname().machine, "os_cpu_count": os.cpu_count()}
+           "cpu": cpu_model(), "os_cpu_count": os.cpu_count()}
     if extras:
         out.update(cpu_extras())
     return out
@@ -439,17 +512,49 @@ def cpu_extras():
 
 
 def run_reference(args):
+    """The reference arm of this tier: the CPU oracle (oracle/, as it stands) on the host cores, on a bounded
+    sample of the same workload (same N, M, media and state recipe; a small Kuhn mesh), W untimed + K timed
+    LSRK45 steps.  ms_per_step is the MEASURED time of one step of that sample (not extrapolated)."""
+    import threadpoolctl
+
+    from oracle.acoustic import AcousticOracle
+    from workloads import kuhn, media, states
+
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cb = cpu_baseline(args.N, args.M, args.cpu_seconds)
-    wname = f"config{args.config} (oracle on a bounded sample: {cb['sample']})"
-    per_step_ms = 4.0 * 6 * args.n_cubes ** 3 * comb(args.N + 3, 3) * 5 / cb["value"] * 1e3
-    out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-           "config": {"workload": wname, "N": args.N, "M": args.M},
-           "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+    N, M = args.N, args.M
+    n = 3 if N >= 7 else 4
+    v, e = kuhn.kuhn_mesh(n)
+    cf = {5: media.c2_smooth(1.0), 3: media.c2_smooth(8.0), 4: media.c2_layered()}.get(args.config, media.c2_smooth(1.0))
+    c2 = media.project_c2(v, e, cf, M)
+    Q = states.gaussian_pulse(v, e, N)
+    t0 = time.perf_counter()
+    o = AcousticOracle(v, e, N, M, c2)
+    setup = time.perf_counter() - t0
+    res = np.zeros_like(Q)
+    dt = 0.5 * kuhn.min_height(v, e) / (np.sqrt(float(c2.max())) * (N + 1) ** 2)
+    for i in range(args.warmup):
+        o.step(Q, res, i * dt, dt)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        o.step(Q, res, (args.warmup + i) * dt, dt)
+    el = time.perf_counter() - t0
+    Np = comb(N + 3, 3)
+    value = 4.0 * len(e) * Np * 5 * args.steps / el
+    info = threadpoolctl.threadpool_info()
+    cores = max([i.get("num_threads", 1) for i in info] + [1])
+    sample = (f"{args.warmup} warm-up + {args.steps} timed LSRK45 steps of the CPU oracle on a {len(e)}-tet Kuhn "
+              f"mesh (n={n}; the GPU arm runs {6 * args.n_cubes ** 3:,} tets per GPU), N={N}, M={M}, config-"
+              f"{args.config} media, Gaussian pulse, fp64 numpy/BLAS; table setup {setup:.1f}s excluded")
+    cb = {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample, "cpu": cpu_model(),
+          "os_cpu_count": os.cpu_count()}
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"config{args.config} sample: {len(e)} tets (n={n}), N={N}, M={M}",
+                      "N": N, "M": M, "K_total": len(e), "same_size_as_gpu_arm": False},
+           "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                                        "d2h_bytes_per_step": 0}, "gpu_launches": 0}
     print(json.dumps(out), flush=True)
 
@@ -471,7 +576,14 @@ def main():
     ap.add_argument("--e2e-random", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--sweep-warmup", type=int, default=3)
+    ap.add_argument("--sweep-steps", type=int, default=10)
+    ap.add_argument("--no-config4", action="store_true", help="skip the config-4 fp64/fp32 extra lines")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world and not (args.gpus == 1 and world == 1):
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 runs with "
+                         f"python -m torch.distributed.run --nproc-per-node {args.gpus} bench.py --gpus {args.gpus}")
     defaults = {5: (7, 4, 88), 3: (7, 7, 44), 4: (5, 3, 56)}
     dN, dM, dn = defaults.get(args.config, (7, 4, 88))
     args.N = args.N if args.N is not None else dN

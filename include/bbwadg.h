@@ -92,7 +92,13 @@ typedef struct {
   int partition[3];      /* cut counts per axis for the recursive coordinate bisection
                             (product must equal world_size); {0,0,0} = automatic */
   int check_c2;          /* 1 (default): reject non-positive c^2_M at setup */
-  int reserved[7];
+  int reserved0;
+  const int64_t* c2_gids; /* optional (multi-GPU memory): when non-NULL, c2_coeffs of bbwadg_setup holds
+                             c2_rows rows, row i for global element c2_gids[i] (e.g. this rank's elements
+                             from bbwadg_partition_plan); every element the rank owns must be present
+                             (else BBWADG_ERR_INVALID_ARG).  NULL: c2_coeffs is [K][Mp] in global order */
+  int64_t c2_rows;
+  int reserved[4];
 } bbwadg_options;
 
 typedef struct {
@@ -111,13 +117,14 @@ typedef struct {
   double time;
 } bbwadg_info;
 
-/* Fill defaults (F64, tau 1/1, device 0, own stream, single GPU, check_c2). */
+/* Fill defaults (F64, tau 1/1, device 0, cuda_stream NULL = the legacy default stream, single GPU, check_c2). */
 void bbwadg_default_options(bbwadg_options* opts);
 
 /* Build the context: validate and partition the mesh, compute geometric
  * factors, build per-(N,M) operator tables, upload everything to the device.
  *   c2_coeffs: host [K][Mp] degree-M Bernstein coefficients of c^2 per element
- *              (global element order), Mp = (M+1)(M+2)(M+3)/6.
+ *              (global element order), Mp = (M+1)(M+2)(M+3)/6; or, with
+ *              opts->c2_gids, [c2_rows][Mp] rows for those global element ids only.
  * The state is zero after setup. */
 bbwadg_status bbwadg_setup(const bbwadg_mesh* mesh, int N, int M, const double* c2_coeffs,
                            const bbwadg_options* opts, bbwadg_ctx* out);

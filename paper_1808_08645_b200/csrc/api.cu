@@ -1,6 +1,7 @@
 // extern "C" implementation of include/bbwadg.h.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges per RK stage / halo (nsys, ncu --nvtx)
 
 #include <algorithm>
 #include <cmath>
@@ -131,10 +132,10 @@ void fill_args(bbwadg_ctx c, StageArgs<R>& a) {
 
 // Launch one kernel pass over local elements [b, e).
 bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e, double rk_a,
-                          double rk_b, double dt, double tstage) {
+                          double rk_b, double dt, double tstage, int grid_cap = 0) {
   if (e <= b) return BBWADG_OK;
   int64_t nb = (e - b + c->ks.elems_per_cta - 1) / c->ks.elems_per_cta;
-  int grid = (int)std::min<int64_t>(nb, c->grid);
+  int grid = (int)std::min<int64_t>(nb, grid_cap > 0 ? grid_cap : c->grid);
   cudaError_t err;
   if (c->dtype == BBWADG_F64) {
     StageArgs<double> a;
@@ -176,14 +177,20 @@ const uint16_t* fnode_ptr(bbwadg_ctx c) {
   return reinterpret_cast<const uint16_t*>(static_cast<const uint8_t*>(c->d_tab) + L.fnode);
 }
 
+struct NvtxRange {  // RAII NVTX range (no-op without a tool attached)
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // NCCL halo for source state Q: pack on the comm stream, grouped send/recv, event.
 bbwadg_status halo_nccl(bbwadg_ctx c, const void* Q) {
+  NvtxRange range("bbwadg halo (pack + NCCL send/recv)");
   const Part& P = c->part;
   const int64_t nsend = P.send_off.back();
   CUDA_TRY(c, cudaEventRecord(c->ev_ready, c->stream));
   CUDA_TRY(c, cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-  CUDA_TRY(c, c->ks.launch_pack(Q, c->d_sendfaces, (int)nsend, fnode_ptr(c), c->d_send, c->comm_stream));
-  const size_t per_face = 4 * (size_t)c->Nfp;
+  CUDA_TRY(c, c->ks.launch_pack(Q, c->d_geo, c->d_sendfaces, (int)nsend, fnode_ptr(c), c->d_send, c->comm_stream));
+  const size_t per_face = 2 * (size_t)c->Nfp;  // p and u.n per face node (Eq. sdf needs only [[p]], n.[[u]])
   int dt = c->dtype == BBWADG_F64 ? nccl::kDouble : nccl::kFloat;
   if (nccl::group_start() != 0) return fail(c, BBWADG_ERR_NCCL, "ncclGroupStart failed");
   for (int r = 0; r < P.nparts; ++r) {
@@ -208,11 +215,16 @@ bbwadg_status halo_nccl(bbwadg_ctx c, const void* Q) {
 // One pass (stage or rhs) over all local elements including the halo exchange when partitioned.
 bbwadg_status full_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, double rk_a, double rk_b, double dt,
                         double tstage) {
+  static const char* kNames[3] = {"bbwadg stage (LSRK)", "bbwadg rhs", "bbwadg wadg_apply"};
+  NvtxRange range(kNames[mode < 0 || mode > 2 ? 0 : mode]);
   const Part& P = c->part;
   if (P.nparts > 1 && c->comm) {
     bbwadg_status s = halo_nccl(c, Qin);
     if (s) return s;
-    s = launch_pass(c, mode, Qin, Qout, 0, P.n_interior, rk_a, rk_b, dt, tstage);
+    // the persistent interior pass leaves two SMs' worth of CTAs free, so the pack and NCCL kernels on
+    // the comm stream run concurrently with it (full occupancy would hold them back until it drains)
+    const int cap = std::max(c->ks.blocks_per_sm(), c->grid - 2 * c->ks.blocks_per_sm());
+    s = launch_pass(c, mode, Qin, Qout, 0, P.n_interior, rk_a, rk_b, dt, tstage, cap);
     if (s) return s;
     CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
     return launch_pass(c, mode, Qin, Qout, P.n_interior, P.K_local, rk_a, rk_b, dt, tstage);
@@ -333,13 +345,34 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   // per-element inputs in local order
   const int64_t KL = P.K_local;
   std::vector<double> geo(12 * KL), c2l((size_t)KL * c->Mp);
+  // c^2 rows: global order, or only the listed global ids (o.c2_gids, sorted lookup)
+  std::vector<std::pair<int64_t, int64_t>> c2map;
+  if (o.c2_gids) {
+    c2map.resize(o.c2_rows);
+    for (int64_t r = 0; r < o.c2_rows; ++r) c2map[r] = {o.c2_gids[r], r};
+    std::sort(c2map.begin(), c2map.end());
+  }
+  std::vector<int64_t> c2row(KL);
+  for (int64_t i = 0; i < KL; ++i) {
+    if (!o.c2_gids) {
+      c2row[i] = P.gid[i];
+      continue;
+    }
+    auto it = std::lower_bound(c2map.begin(), c2map.end(), std::make_pair(P.gid[i], (int64_t)-1));
+    if (it == c2map.end() || it->first != P.gid[i]) {
+      std::ostringstream os;
+      os << "c2_gids lacks global element " << P.gid[i] << " owned by rank " << rank;
+      return fail(nullptr, BBWADG_ERR_INVALID_ARG, os.str());
+    }
+    c2row[i] = it->second;
+  }
   C2Checker chk(M);
   int64_t bad = -1;
   double badv = 0;
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < KL; ++i) {
     element_gradients(g, P.gid[i], &geo[12 * i]);
-    const double* ci = c2 + (size_t)P.gid[i] * c->Mp;
+    const double* ci = c2 + (size_t)c2row[i] * c->Mp;
     std::memcpy(&c2l[(size_t)i * c->Mp], ci, sizeof(double) * c->Mp);
     if (o.check_c2) {
       // convex hull property: all Bernstein coefficients > 0 => c^2_M > 0 on the element
@@ -382,7 +415,7 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
     CUDA_TRY(c.get(), cudaMemset(c->d_ptime, 0, 32 * sizeof(unsigned long long)));
   }
   const int64_t nghost = P.num_ghost(), nsend = P.send_off.empty() ? 0 : P.send_off.back();
-  const size_t per_face = 4 * (size_t)c->Nfp * c->rb;
+  const size_t per_face = 2 * (size_t)c->Nfp * c->rb;  // halo: p and u.n per face node
   if (nghost > 0) CUDA_TRY(c.get(), cudaMalloc(&c->d_ghost, nghost * per_face));
   if (nsend > 0) {
     CUDA_TRY(c.get(), cudaMalloc(&c->d_send, nsend * per_face));
@@ -441,11 +474,12 @@ bbwadg_status bbwadg_setup(const bbwadg_mesh* mesh, int N, int M, const double* 
     return fail(nullptr, BBWADG_ERR_INVALID_ARG, "rank/world_size invalid");
   if (o.world_size > 1 && !o.nccl_unique_id)
     return fail(nullptr, BBWADG_ERR_INVALID_ARG, "world_size > 1 needs nccl_unique_id");
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(nullptr, BBWADG_ERR_NO_DEVICE, "no CUDA device");
+  // argument and mesh validation first (host only), then the device
   GlobalMesh g;
   bbwadg_status s = prepare_global(mesh, N, M, c2_coeffs, &o, o.world_size, g);
   if (s) return s;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(nullptr, BBWADG_ERR_NO_DEVICE, "no CUDA device");
   s = setup_one(g, N, M, c2_coeffs, o, o.rank, o.world_size, nullptr, out);
   if (s) return s;
   bbwadg_ctx c = *out;
@@ -461,9 +495,14 @@ bbwadg_status bbwadg_setup(const bbwadg_mesh* mesh, int N, int M, const double* 
       *out = nullptr;
       return fail(nullptr, BBWADG_ERR_NCCL, "ncclCommInitRank failed");
     }
-    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+    cudaError_t ce = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
+    if (ce != cudaSuccess) {  // never hand out a half-built context
+      bbwadg_destroy(c);
+      *out = nullptr;
+      return fail(nullptr, BBWADG_ERR_CUDA, std::string("comm stream/events: ") + cudaGetErrorString(ce));
+    }
   }
   return BBWADG_OK;
 }
@@ -485,8 +524,11 @@ bbwadg_status bbwadg_setup_group(const bbwadg_mesh* mesh, int N, int M, const do
     bbwadg_ctx c = nullptr;
     s = setup_one(g, N, M, c2_coeffs, o, r, nparts, shared, &c);
     if (s) {
-      for (auto p : grp->parts) bbwadg_destroy(p);
-      delete grp;
+      // destroy the members built so far (the last one frees the group) and clear the caller's handles
+      std::vector<bbwadg_ctx> built = grp->parts;
+      for (auto p : built) bbwadg_destroy(p);
+      if (built.empty()) delete grp;
+      for (int j = 0; j < nparts; ++j) out[j] = nullptr;
       return s;
     }
     if (r == 0) {
@@ -571,11 +613,12 @@ bbwadg_status bbwadg_group_step(bbwadg_ctx* ctxs, int n, double t, double dt) {
     for (int r = 0; r < n; ++r) {
       bbwadg_ctx c = ctxs[r];
       int64_t ns = c->part.send_off.back();
-      CUDA_TRY(c, c->ks.launch_pack(c->d_Q[c->cur], c->d_sendfaces, (int)ns, fnode_ptr(c), c->d_send, c->stream));
+      CUDA_TRY(c, c->ks.launch_pack(c->d_Q[c->cur], c->d_geo, c->d_sendfaces, (int)ns, fnode_ptr(c), c->d_send,
+                                    c->stream));
     }
     for (int r = 0; r < n; ++r) {
       bbwadg_ctx c = ctxs[r];
-      const size_t per_face = 4 * (size_t)c->Nfp * c->rb;
+      const size_t per_face = 2 * (size_t)c->Nfp * c->rb;
       for (int q = 0; q < n; ++q) {
         int64_t nr = c->part.recv_off[q + 1] - c->part.recv_off[q];
         if (nr == 0) continue;
@@ -624,6 +667,14 @@ bbwadg_status bbwadg_run(bbwadg_ctx c, double t0, double dt, int64_t nsteps) {
   int flag = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->comm) {
+    const int ne = nccl::async_error(c->comm);
+    if (ne != 0 && ne != 7) {
+      std::ostringstream os;
+      os << "NCCL asynchronous error " << ne << " (" << nccl::last_error(c->comm) << ")";
+      return fail(c, BBWADG_ERR_NCCL, os.str());
+    }
+  }
   if (flag) {
     std::ostringstream os;
     os << "non-finite state after step " << c->steps;
@@ -635,6 +686,10 @@ bbwadg_status bbwadg_run(bbwadg_ctx c, double t0, double dt, int64_t nsteps) {
 bbwadg_status bbwadg_synchronize(bbwadg_ctx c) {
   if (!c) return fail(c, BBWADG_ERR_INVALID_ARG, "null ctx");
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->comm) {
+    const int ne = nccl::async_error(c->comm);
+    if (ne != 0 && ne != 7) return fail(c, BBWADG_ERR_NCCL, std::string("NCCL asynchronous error: ") + nccl::last_error(c->comm));
+  }
   return BBWADG_OK;
 }
 

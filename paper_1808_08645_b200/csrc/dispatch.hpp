@@ -8,8 +8,9 @@ namespace bbw {
 struct KernelSet {
   // args points to StageArgs<double> or StageArgs<float>
   cudaError_t (*launch_stage)(const void* args, int grid, cudaStream_t s) = nullptr;
-  cudaError_t (*launch_pack)(const void* Q, const int* faces, int nfaces, const uint16_t* fnode, void* buf,
-                             cudaStream_t s) = nullptr;
+  // halo pack: p and u.n_sender per send-face node ([faces][2][Nfp]); geo = grad(lambda) [K][12]
+  cudaError_t (*launch_pack)(const void* Q, const void* geo, const int* faces, int nfaces, const uint16_t* fnode,
+                             void* buf, cudaStream_t s) = nullptr;
   cudaError_t (*prepare)() = nullptr;  // set smem attributes
   int (*blocks_per_sm)() = nullptr;
   int smem_bytes = 0, elems_per_cta = 0, threads = 0;

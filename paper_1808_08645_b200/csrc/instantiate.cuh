@@ -18,13 +18,14 @@ struct Inst {
     stage_kernel<C, R><<<grid, C::T, C::SMEM_BYTES, s>>>(a);
     return cudaGetLastError();
   }
-  static cudaError_t pack(const void* Q, const int* faces, int nfaces, const uint16_t* fnode, void* buf,
-                          cudaStream_t s) {
+  static cudaError_t pack(const void* Q, const void* geo, const int* faces, int nfaces, const uint16_t* fnode,
+                          void* buf, cudaStream_t s) {
     if (nfaces <= 0) return cudaSuccess;
-    long long total = (long long)nfaces * 4 * cnp2(N);
+    long long total = (long long)nfaces * cnp2(N);
     int grid = (int)((total + 255) / 256);
     if (grid > 4 * 148) grid = 4 * 148;
-    pack_kernel<N, R><<<grid, 256, 0, s>>>(static_cast<const R*>(Q), faces, nfaces, fnode, static_cast<R*>(buf));
+    pack_kernel<N, R><<<grid, 256, 0, s>>>(static_cast<const R*>(Q), static_cast<const R*>(geo), faces, nfaces, fnode,
+                                           static_cast<R*>(buf));
     return cudaGetLastError();
   }
   static int blocks() {

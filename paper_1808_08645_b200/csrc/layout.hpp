@@ -22,6 +22,7 @@ __host__ __device__ constexpr int al16(int x) { return (x + 15) & ~15; }
 struct TabLayout {
   // byte offsets of the sections
   int vg, ve, red, upw, lg, trired, triele, fnode, nbrvol, nbrface, rowdec, padoff, rowlen;
+  int shd, shu, sho, shw, shs;  // shell-order ("triple") tables of the WADG projection
   int s_invfacN, s_facN, s_invfac2N, s_outN, s_invfacM, s_post, s_invfacNm1, s_cfac, s_invf2, s_cf2, s_rowpost;
   int total;
 };
@@ -69,8 +70,27 @@ __host__ __device__ constexpr TabLayout tab_layout(int N, int M, int RB) {
   L.s_invf2 = o;    o = al16(o + RB * lnp2(N - 1));
   L.s_cf2 = o;      o = al16(o + RB * lnp2(N));
   L.s_rowpost = o;  o = al16(o + RB * lnp2(N + M));
+  L.shd = o;        o = al16(o + 4 * lnp3(N + M - 1 > N ? N + M - 1 : N));
+  L.shu = o;        o = al16(o + 4 * lnp3(N));
+  L.sho = o;        o = al16(o + 4 * lnp3(N));
+  L.shw = o;        o = al16(o + RB * lnp3(N));
+  L.shs = o;        o = al16(o + RB * lnp3(N));
   L.total = o;
   return L;
+}
+
+// Shell order ("triple" ownership of the WADG projection): the multi-indices t = (a1,a2,a3)
+// of every degree n <= N+M are enumerated by d = |t| (shell), then a3, then a2:
+//   f(t) = Np(d-1) + a3 (2d+3-a3)/2 + a2,
+// the same index at EVERY degree (a0 = n - d is implied), so degree n is the prefix f < Np(n).
+// SHD[f] = f(t+e1) | (d+2-a3) << 16                      (f(t+e2) = f(t+e1)+1, f(t+e3) = f(t+e1)+d+2-a3)
+// SHU[f] = (f(t-e1)+1) | (f(t-e2)+1) << 8 | (f(t-e3)+1) << 16 | d << 24     (0: t-e_j does not exist)
+// SHO[a] = shell index f of the canonical degree-N coefficient a;  SHW[f] = 1/(a1! a2! a3!)^2;
+// SHS[f] = a!/N!, a0 = N - d
+__host__ __device__ constexpr int shell_of(int f) {
+  int d = 0;
+  while (lnp3(d) <= f) ++d;
+  return d;  // shell d: Np(d-1) <= f < Np(d)
 }
 
 // offset (in entries) of degree n inside RED (degrees 1..N+M) and UPW (degrees 1..N)

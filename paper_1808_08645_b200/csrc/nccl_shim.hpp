@@ -23,6 +23,7 @@ typedef int (*SendFn)(const void*, size_t, int, int, Comm, cudaStream_t);
 typedef int (*RecvFn)(void*, size_t, int, int, Comm, cudaStream_t);
 typedef int (*GroupFn)();
 typedef const char* (*LastErrorFn)(Comm);
+typedef int (*AsyncErrorFn)(Comm, int*);
 
 struct Api {
   void* handle = nullptr;
@@ -33,6 +34,7 @@ struct Api {
   RecvFn recv = nullptr;
   GroupFn groupStart = nullptr, groupEnd = nullptr;
   LastErrorFn lastError = nullptr;
+  AsyncErrorFn asyncError = nullptr;
 };
 
 inline Api& api() {
@@ -65,6 +67,7 @@ inline bool load(std::string& why) {
   a.groupStart = (GroupFn)dlsym(a.handle, "ncclGroupStart");
   a.groupEnd = (GroupFn)dlsym(a.handle, "ncclGroupEnd");
   a.lastError = (LastErrorFn)dlsym(a.handle, "ncclGetLastError");
+  a.asyncError = (AsyncErrorFn)dlsym(a.handle, "ncclCommGetAsyncError");
   if (!a.getUniqueId || !a.commInitRank || !a.send || !a.recv || !a.groupStart || !a.groupEnd) {
     why = "libnccl.so.2 lacks required symbols";
     return false;
@@ -89,6 +92,12 @@ inline int recv(void* b, size_t n, int dt, int peer, Comm c, cudaStream_t s) { r
 inline int group_start() { return api().groupStart(); }
 inline int group_end() { return api().groupEnd(); }
 inline const char* last_error(Comm c) { return api().lastError ? api().lastError(c) : ""; }
+// ncclCommGetAsyncError: 0 = ncclSuccess, 7 = ncclInProgress (non-blocking init), else a failure
+inline int async_error(Comm c) {
+  int e = 0;
+  if (!api().asyncError || api().asyncError(c, &e) != 0) return 0;
+  return e;
+}
 
 }  // namespace nccl
 }  // namespace bbw

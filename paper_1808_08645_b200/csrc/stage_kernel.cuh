@@ -50,7 +50,7 @@ struct StageArgs {
   const R* geo;        // [K][12]: grad(lambda_0..3)
   const int* nbr;      // [K][4]
   const uint8_t* code; // [K][4] = 6 f' + sigma
-  const R* ghost;      // [slots][4][NFP]
+  const R* ghost;      // [slots][2][NFP]: p and u.n_sender at the sender's face nodes (halo, Eq. sdf)
   const R* src;        // [K][NP] or null
   const uint8_t* tab;  // table blob (layout.hpp)
   long long elem_begin, elem_end;
@@ -73,6 +73,10 @@ __host__ __device__ constexpr int default_et(int N) { return N > 0 ? 1 : 1; }
 // minimum resident CTAs per SM for __launch_bounds__ (caps registers at 65536 / (T * MINB)); A/B-measured
 // (scripts/ab_minb.sh): 5 for N = 4, 5 (+3.6 %, +2..3 %), 4 elsewhere (N=6: -5.7 %, N=7: -15 % at 5)
 __host__ __device__ constexpr int default_minb(int N) { return (N == 4 || N == 5) ? 5 : 4; }
+
+#ifndef BBW_TRIPLE
+#define BBW_TRIPLE 2  // shell-order ownership of the WADG projection: 1 always, 0 never, 2 where it measured faster
+#endif
 
 template <int N_, int M_, typename R>
 struct StageCfg {
@@ -129,7 +133,20 @@ struct StageCfg {
   static constexpr int WSIZE = !ALIAS ? WSIZE_V3
                                       : cmax(cmax(W_LEV + LEVSZ, W_P + (M >= 1 ? NPH1 : 0)), W_H + NPH) - O_X;
   static __host__ __device__ constexpr int lev(int n) { return ALIAS ? W_LEV + lnp4(n - 1) + n + 1 : W_LEV + lnp4(n - 1); }
-  static constexpr int PER_E = rup(O_X + cmax(XSIZE + YSIZE, WSIZE), VEC);
+  // shell-order ("triple") WADG layout (BBW_TRIPLE): product output h (degree N+M) at T_H, the G ping-pong
+  // partner at T_P, the N+1 levels of the telescoping sweeps at tlev(n) (each preceded by a zero slot),
+  // placed over a region that is dead when G's last step writes level N
+  static constexpr int T_H = O_X, T_P = T_H + NPH, T_LEVSZ = NP4 + N + 1;
+  static constexpr bool T_LAST_FROM_P = (M >= 1) && ((M - 1) % 2 == 1);
+  static constexpr int T_LVB = (M == 0) ? O_X
+                               : (M == 1) ? T_P
+                               : T_LAST_FROM_P ? (T_LEVSZ <= NPH ? T_H : T_P + NPH1)
+                                               : (T_LEVSZ <= NPH1 ? T_P : T_P + NPH1);
+  static __host__ __device__ constexpr int tlev(int n) { return T_LVB + lnp4(n - 1) + n + 1; }
+  static constexpr int T_WSIZE = cmax(cmax(T_LVB + T_LEVSZ, T_P + (M >= 1 ? NPH1 : 0)), T_H + NPH) - O_X;
+  // A/B (scripts/gpu_r2_full.sh): +18 % at N = M = 9, +2 % at (5,3), -3 % at (7,4) and (3,1) -> used for N+M >= 14
+  static constexpr bool TRIPLE = BBW_TRIPLE == 1 ? true : BBW_TRIPLE == 0 ? false : (N + M >= 14);
+  static constexpr int PER_E = rup(O_X + cmax(XSIZE + YSIZE, TRIPLE ? T_WSIZE : WSIZE), VEC);
   static constexpr int EB = PER_E * RB;  // element stride in bytes
   static constexpr int GB = ET * EB;     // group stride in bytes
   static constexpr int SMEM_BYTES = G * GB + 8 * G;  // + one mbarrier per group (TMA bulk loads)
@@ -218,12 +235,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 #ifndef BBW_PF  // L2 prefetch of the next batch: no speed-up measured, +7 GB DRAM reads per config-5 stage
 #define BBW_PF 0
+#endif
+#ifndef BBW_M0_FAST
+#define BBW_M0_FAST 1  // M = 0: WADG = multiplication by the constant c^2 (skip the product and the sweeps)
+#endif
+#ifndef BBW_LSRK_TMEM
+#define BBW_LSRK_TMEM 0
 #endif
 #ifndef BBW_LSRK_REG
 #define BBW_LSRK_REG 1
@@ -312,6 +336,89 @@ __device__ __forceinline__ void static_for(F&& f) {
   if constexpr ((STEP > 0 && I < END) || (STEP < 0 && I > END)) {
     f(std::integral_constant<int, I>{});
     static_for<I + STEP, END, STEP>(f);
+  }
+}
+
+// ---- TMEM (tensor memory) as lane-private storage for the LSRK state (BBW_LSRK_TMEM): each lane keeps
+// its Q_in copy and residual in its own TMEM lane between the batch start and phases E / J, so those 64
+// registers are free for the sparse phases (SASS STTM / LDTM; TMEM traffic does not use L1 wavefronts)
+template <int NW>
+__device__ __forceinline__ void tm_st(uint32_t taddr, const uint32_t* v);
+template <>
+__device__ __forceinline__ void tm_st<8>(uint32_t t, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(t), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_st<16>(uint32_t t, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(t),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+template <int NW>
+__device__ __forceinline__ void tm_ld(uint32_t taddr, uint32_t* v);
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t t, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(t)
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld<16>(uint32_t t, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(t)
+      : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// store / load n reals (n*RB/4 32-bit columns, in chunks of 16 / 8 columns) at column offset col
+template <typename R, int NR>
+__device__ __forceinline__ void tm_store_reals(uint32_t taddr, int col0, const R* x) {
+  constexpr int NWD = NR * (int)sizeof(R) / 4;
+  uint32_t w[NWD];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    if constexpr (sizeof(R) == 8) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong((double)x[i]);
+      w[2 * i] = (uint32_t)b;
+      w[2 * i + 1] = (uint32_t)(b >> 32);
+    } else {
+      w[i] = __float_as_uint((float)x[i]);
+    }
+  }
+  static_assert(NWD % 8 == 0, "TMEM chunks of 8 columns");
+  static_for<0, NWD, 8>([&](auto c) {
+    constexpr int c0 = decltype(c)::value;
+    // x16 chunks where 16 columns remain, the tail (if any) as x8; c0 = 16 j + 8 is covered by the x16 at 16 j
+    if constexpr (c0 % 16 == 0 && c0 + 16 <= NWD) tm_st<16>(taddr + col0 + c0, w + c0);
+    else if constexpr (!(c0 % 16 == 8 && c0 + 8 <= NWD)) tm_st<8>(taddr + col0 + c0, w + c0);
+  });
+}
+template <typename R, int NR>
+__device__ __forceinline__ void tm_load_reals(uint32_t taddr, int col0, R* x) {
+  constexpr int NWD = NR * (int)sizeof(R) / 4;
+  uint32_t w[NWD];
+  static_for<0, NWD, 8>([&](auto c) {
+    constexpr int c0 = decltype(c)::value;
+    // x16 chunks where 16 columns remain, the tail (if any) as x8; c0 = 16 j + 8 is covered by the x16 at 16 j
+    if constexpr (c0 % 16 == 0 && c0 + 16 <= NWD) tm_ld<16>(taddr + col0 + c0, w + c0);
+    else if constexpr (!(c0 % 16 == 8 && c0 + 8 <= NWD)) tm_ld<8>(taddr + col0 + c0, w + c0);
+  });
+  tm_wait_ld();
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    if constexpr (sizeof(R) == 8) {
+      x[i] = (R)__longlong_as_double((long long)(((unsigned long long)w[2 * i + 1] << 32) | w[2 * i]));
+    } else {
+      x[i] = (R)__uint_as_float(w[i]);
+    }
   }
 }
 
@@ -413,9 +520,128 @@ __device__ __forceinline__ void zero_region(char* gb, int q, int off, int cnt) {
   }
 }
 
+// 1/((m)!)^2 for a runtime m known to lie in [LO, HI] (select chain over compile-time constants)
+template <typename R, int LO, int HI>
+__device__ __forceinline__ R inv_fact2_sel(int m) {
+  R r = R(1.0 / fact2c(LO > 0 ? LO : 0));
+  static_for<LO + 1, HI + 1, 1>([&](auto mc) {
+    constexpr int mm = decltype(mc)::value;
+    if (m == mm) r = R(1.0 / fact2c(mm));
+  });
+  return r;
+}
+
+// G, H, I of the telescoping projection (Eq. telescope) with SHELL-ORDER ownership
+// (layout.hpp): lane q owns the multi-indices t with shell index f = q + TG k at every degree, keeps its
+// own value of the current level in a register (the e_0 term of every one-degree reduction/elevation),
+// and reads only the three other stencil operands from shared memory, at offsets that are the same for
+// every degree (SHD/SHU, loaded once per element); outputs are stored at f (contiguous, conflict-free).
+//   G/H: u_{n-1}[t] = u_n[t] + u_n[t+e1] + u_n[t+e2] + u_n[t+e3]          (factorial-scaled)
+//   I:   b_n[t]   = b_{n-1}[t] + sum_j b_{n-1}[t-e_j] + gam_n u_n[t] / (a!)^2,   b_0 = gam_0 u_0
+// On return ob[k] holds b_N at f = q + TG k (k < KO).
+template <class C, typename R>
+__device__ __forceinline__ void tri_projection(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync,
+                                               long long& pt_prev, R* ob) {
+  constexpr int N = C::N, M = C::M, NP = C::NP, RB = C::RB, TG = C::TG, KO = C::KO;
+  constexpr TabLayout L = tab_layout(N, M, RB);
+  const uint8_t* tab = A.tab;
+  constexpr int NOUT0 = cnp3(cmax(N + M - 1, N - 1));
+  constexpr int KD = (NOUT0 + TG - 1) / TG;
+  const uint32_t* shd = reinterpret_cast<const uint32_t*>(tab + L.shd);
+  uint32_t sd[KD];
+#pragma unroll
+  for (int k = 0; k < KD; ++k) sd[k] = __ldg(shd + cmin(q + TG * k, NOUT0 - 1));
+  R own[KD];
+  // one-degree reduction of the level at SRC (degree n) into DST (degree n-1), own values in registers
+  auto reduce = [&](auto srcc, auto dstc, auto nc, auto firstc) {
+    constexpr int SRC = decltype(srcc)::value, DST = decltype(dstc)::value, n = decltype(nc)::value;
+    constexpr bool FIRST = decltype(firstc)::value;
+    constexpr int NOUT = cnp3(n - 1), K = (NOUT + TG - 1) / TG;
+    static_for<0, K, 1>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      const int f = q + TG * k;
+      if ((NOUT % TG == 0 && k < K) || f < NOUT) {
+        const int f1 = (int)(sd[k] & 0xFFFF), de = (int)(sd[k] >> 16);
+        const char* sp = gb + (SRC + f1) * RB;
+        if constexpr (FIRST) own[k] = ld<R>(gb + (SRC + f) * RB);
+        const R v = (own[k] + ld<R>(sp)) + (ld<R>(sp + RB) + ld<R>(sp + de * RB));
+        st<R>(gb + (DST + f) * RB, v);
+        own[k] = v;
+      }
+    });
+  };
+  // G: M reductions N+M -> N (ping-pong T_H <-> T_P; the last lands in level N)
+  static_for<N + M, N, -1>([&](auto nc) {
+    constexpr int n = decltype(nc)::value;
+    constexpr int k = N + M - n;
+    constexpr int SRC = (k % 2 == 0) ? C::T_H : C::T_P;
+    constexpr int DST = (n - 1 == N) ? C::tlev(N) : ((k % 2 == 0) ? C::T_P : C::T_H);
+    reduce(std::integral_constant<int, SRC>{}, std::integral_constant<int, DST>{}, nc,
+           std::integral_constant<bool, k == 0>{});
+    sync();
+    BBW_PT(7);
+  });
+  // zero slots in front of levels 0..N-1, read by the upward sweep for missing t - e_j (after G: the
+  // level region may alias the G buffers)
+  if (q < N) st<R>(gb + (C::tlev(q) - 1) * RB, R(0));
+  // H: downward reductions level n -> n-1 (levels kept for I)
+  static_for<N, 0, -1>([&](auto nc) {
+    constexpr int n = decltype(nc)::value;
+    reduce(std::integral_constant<int, C::tlev(n)>{}, std::integral_constant<int, C::tlev(n - 1)>{}, nc,
+           std::integral_constant<bool, M == 0 && n == N>{});
+    sync();
+    BBW_PT(8);
+  });
+  // I: upward, in place (b_n overwrites u_n)
+  const uint32_t* shu = reinterpret_cast<const uint32_t*>(tab + L.shu);
+  const R* shw = reinterpret_cast<const R*>(tab + L.shw);
+  uint32_t su[KO];
+  R wk[KO];
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int fc = cmin(q + TG * k, NP - 1);
+    su[k] = __ldg(shu + fc);
+    wk[k] = __ldg(shw + fc);
+  }
+  if (q == 0) {
+    const R b0 = A.gam[0] * ld<R>(gb + C::tlev(0) * RB);
+    st<R>(gb + C::tlev(0) * RB, b0);
+    ob[0] = b0;
+  }
+  sync();
+  static_for<1, N + 1, 1>([&](auto nc) {
+    constexpr int n = decltype(nc)::value;
+    constexpr int NOUT = cnp3(n), NPREV = cnp3(n - 1), K = (NOUT + TG - 1) / TG;
+    constexpr int BP = C::tlev(n - 1) - 1;  // zero slot of level n-1; SHU offsets are f + 1
+    const R gn = A.gam[n];
+    static_for<0, K, 1>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      const int f = q + TG * k;
+      if ((NOUT % TG == 0 && k < K) || f < NOUT) {
+        constexpr int DLO = shell_of(TG * k), DHI = shell_of(cmin(TG * k + TG, NOUT) - 1);
+        const uint32_t u = su[k];
+        const int d = (int)(u >> 24);
+        const R w = gn * wk[k] * inv_fact2_sel<R, n - DHI, n - DLO>(n - d);
+        const R un = ld<R>(gb + (C::tlev(n) + f) * RB);
+        R v = (ld<R>(gb + (BP + (int)(u & 0xFF)) * RB) + ld<R>(gb + (BP + (int)((u >> 8) & 0xFF)) * RB)) +
+              ld<R>(gb + (BP + (int)((u >> 16) & 0xFF)) * RB);
+        if constexpr (k * TG < NPREV) {
+          if (f < NPREV) v += ob[k];
+        }
+        v = fma(w, un, v);
+        st<R>(gb + (C::tlev(n) + f) * RB, v);
+        ob[k] = v;
+      }
+    });
+    sync();
+    BBW_PT(9);
+  });
+}
+
 template <class C, typename R>
 __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync,
-                                            long long& pt_prev, R* osc) {
+                                            long long& pt_prev, R* ob) {
+  R* osc = ob;  // v4 path: output scales of J
   constexpr int N = C::N, M = C::M, NP = C::NP, NPH = C::NPH, RB = C::RB, ET = C::ET, EB = C::EB, TG = C::TG;
   constexpr TabLayout L = tab_layout(N, M, RB);
   const uint8_t* tab = A.tab;
@@ -432,6 +658,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   // accumulators are live at once; pass k only holds rows with g2+g3 >= SMIN(k) (ROWDEC is sorted by
   // g2+g3 and permuted only within 32-row blocks), which bounds its compile-time row length.
   {
+    static_assert(ET == 1, "product v5 assumes one element per group batch");
     constexpr int NR = cnp2(N + M), KR = (NR + TG - 1) / TG;
     constexpr int VEC = C::VEC, RS = C::RS, LH = N + M + 1;
     const uint32_t* rowdec = reinterpret_cast<const uint32_t*>(tab + L.rowdec);
@@ -515,31 +742,47 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
       constexpr int AO = prod_acc_off(N + M, TG, k);
       if (actv[k]) {
         const int lg = N + M - g2v[k] - g3v[k] + 1;
+        // TRIPLE: shell index of t = (x, g2, g3): f = Np(d-1) + g3 (2d+3-g3)/2 + g2, d = x + g2 + g3, stepped
+        // down in x; otherwise the canonical degree-(N+M) rank gs + x
+        constexpr int DSTH = (M == 0) ? C::tlev(N) : C::T_H;
+        const int sg = g2v[k] + g3v[k];
+        int dd = LMAX - 1 + sg;
+        int fx = dd * (dd + 1) * (dd + 2) / 6 + g3v[k] * (2 * dd + 3 - g3v[k]) / 2 + g2v[k];
+        int Dn = dd * (dd + 1) / 2;  // Nfp(d-1)
+#define BBW_HSTORE(xx, val)                                        \
+  do {                                                             \
+    if constexpr (C::TRIPLE) st<R>(gb + (DSTH + fx) * RB, (val));   \
+    else st<R>(gb + (C::W_H + gsv[k] + (xx)) * RB, (val));         \
+  } while (0)
+#define BBW_HSTEP()                \
+  do {                             \
+    if constexpr (C::TRIPLE) {     \
+      fx -= Dn + g3v[k];           \
+      Dn -= dd;                    \
+      --dd;                        \
+    }                              \
+  } while (0)
         if constexpr (N + M <= 12) {
           R P = rowfv[k], T = R(lg - (N + M));
           static_for<N + M, -1, -1>([&](auto xc) {
             constexpr int x = decltype(xc)::value;
             if constexpr (x < LMAX) {
-              if (x < lg) {
-#pragma unroll
-                for (int u = 0; u < ET; ++u)
-                  st<R>(gb + (C::W_H + gsv[k] + x) * RB + u * EB, acc[u][AO + x] * (R(fact2c(x)) * P));
-              }
+              if (x < lg) BBW_HSTORE(x, acc[0][AO + x] * (R(fact2c(x)) * P));
+              if constexpr (x > 0) BBW_HSTEP();
             }
             const R Tc = T > R(1) ? T : R(1);
             P *= Tc * Tc;
             T += R(1);
           });
         } else {
-#pragma unroll
-          for (int x = 0; x < LMAX; ++x) {
-            if (x < lg) {
-              const R sp = __ldg(post + gsv[k] + x);
-#pragma unroll
-              for (int u = 0; u < ET; ++u) st<R>(gb + (C::W_H + gsv[k] + x) * RB + u * EB, acc[u][AO + x] * sp);
-            }
-          }
+          static_for<LMAX - 1, -1, -1>([&](auto xc) {
+            constexpr int x = decltype(xc)::value;
+            if (x < lg) BBW_HSTORE(x, acc[0][AO + x] * __ldg(post + gsv[k] + x));
+            if constexpr (x > 0) BBW_HSTEP();
+          });
         }
+#undef BBW_HSTORE
+#undef BBW_HSTEP
       }
     });
   }
@@ -660,6 +903,10 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
 #endif
   sync();
   BBW_PT(6);
+  if constexpr (C::TRIPLE) {
+    tri_projection<C, R>(gb, q, A, sync, pt_prev, ob);
+    return;
+  }
   if constexpr (!C::ALIAS) {
     if (q == 0) {  // zero slots of the upward-sweep ping-pong buffers (may alias the padded rows read above)
 #pragma unroll
@@ -786,12 +1033,33 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
 
   const long long nelem = A.elem_end - A.elem_begin;
   const long long nbatch = (nelem + ET - 1) / ET;
+#define BBW_PA(k) (q + TG * (k))
 #if BBW_TMA && BBW_CPASYNC
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + C::G * C::GB) + grp;
   unsigned mbar_phase = 0;
   if (q == 0) mbar_init(mbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+#endif
+#if BBW_LSRK_TMEM
+  static_assert(ET == 1 && BBW_LSRK_REG, "TMEM LSRK state: one element per batch, register-resident state model");
+  // LSRK state columns: residual at [0, TMW), Q_in copy at [TMW, 2 TMW); TMW = 4 KO reals in 32-bit words,
+  // rounded up to 8 columns; the allocation (power of 2 >= 32) is per CTA, lanes per warp quadrant
+  constexpr int TMR = ((4 * KO * RB / 4 + 7) / 8 * 8) / (RB / 4);  // reals per array, padded
+  constexpr int TMW = TMR * RB / 4;
+  constexpr int TMCOLS = (2 * TMW <= 32) ? 32 : (2 * TMW <= 64) ? 64 : (2 * TMW <= 128) ? 128 : 256;
+  __shared__ uint32_t tmem_base_s;
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&tmem_base_s)),
+                 "r"(TMCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t taddr = tmem_base_s + ((uint32_t)(32 * ((tid >> 5) & 3)) << 16);
 #endif
   // Sub-warp groups (TG < 32) share their warp's synchronisation, so the trip count is uniform per
   // warp: the loop runs over the batch of the warp's first group, idle groups get nE = 0.
@@ -818,8 +1086,8 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int k = 0; k < KO; ++k) {
-            const int a = q + TG * k;
-            rs[u][c][k] = (u < nE && a < NP) ? __ldcs(A.res + (k0 + u) * 4 * NP + c * NP + a) : R(0);
+            const int a = c == 0 ? BBW_PA(k) : q + TG * k;
+            rs[u][c][k] = (u < nE && q + TG * k < NP) ? __ldcs(A.res + (k0 + u) * 4 * NP + c * NP + a) : R(0);
           }
     }
 #else
@@ -1004,12 +1272,12 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
               tuy[k][u] = __ldg(qn + 2 * NP);
               tuz[k][u] = __ldg(qn + 3 * NP);
             } else if (nb < -1) {
+              // partition face: the halo carries p+ and u+.n+ (n+ = the sender's outward normal = -n);
+              // the flux needs only [[p]] and n.[[u]] (Eq. sdf); tux holds u+.n+
               const int fi = __ldg(nbrface + (code % 6) * NFP + i);
-              const R* gh = A.ghost + (long long)(-2 - nb) * 4 * NFP + fi;
+              const R* gh = A.ghost + (long long)(-2 - nb) * 2 * NFP + fi;
               tpp[k][u] = gh[0];
               tux[k][u] = gh[NFP];
-              tuy[k][u] = gh[2 * NFP];
-              tuz[k][u] = gh[3 * NFP];
             }
           }
         }
@@ -1070,7 +1338,8 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
           const char* gs = gb + u * EB + (C::O_GEO + 12 + 4 * f) * RB;
           const R nx = ld<R>(gs), ny = ld<R>(gs + RB), nz = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * cs;
           const R jp = pp - pm;
-          const R jun = nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
+          const R jun = (nb < -1) ? -tux[k][u] - (nx * uxm + ny * uym + nz * uzm)
+                                  : nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
           if (act) {
             st<R>(gb + u * EB + (C::Y_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));
             st<R>(gb + u * EB + (C::Y_F + (2 * f + 1) * NFP + i) * RB, R(0.5) * sc * (A.tau_u * jun - jp));
@@ -1085,9 +1354,21 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int k = 0; k < KO; ++k) {
-            const int a = q + TG * k;
-            qo[u][c][k] = (a < NP) ? ld<R>(gb + u * EB + (C::X_Q + c * NP + a) * RB) : R(0);
+            const int a = c == 0 ? BBW_PA(k) : q + TG * k;
+            qo[u][c][k] = (q + TG * k < NP) ? ld<R>(gb + u * EB + (C::X_Q + c * NP + a) * RB) : R(0);
           }
+#endif
+#if BBW_LSRK_TMEM
+      if (A.mode == 0) {  // park the LSRK state in TMEM until E / J
+        R t0[TMR], t1[TMR];
+#pragma unroll
+        for (int i = 0; i < TMR; ++i) {
+          t0[i] = i < 4 * KO ? rs[0][i / KO][i % KO] : R(0);
+          t1[i] = i < 4 * KO ? qo[0][i / KO][i % KO] : R(0);
+        }
+        tm_store_reals<R, TMR>(taddr, 0, t0);
+        tm_store_reals<R, TMR>(taddr, TMW, t1);
+      }
 #endif
       sync();
       BBW_PT(1);
@@ -1180,6 +1461,18 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         sync();
         BBW_PT(4);
       });
+#if BBW_LSRK_TMEM
+      if (A.mode == 0) {
+        R t0[TMR], t1[TMR];
+        tm_load_reals<R, TMR>(taddr, 0, t0);
+        tm_load_reals<R, TMR>(taddr, TMW, t1);
+#pragma unroll
+        for (int i = 0; i < 4 * KO; ++i) {
+          rs[0][i / KO][i % KO] = t0[i];
+          qo[0][i / KO][i % KO] = t1[i];
+        }
+      }
+#endif
       // ---- E: gather lifts; r''_p += S_p/(a!)^2 (+ source) -> smem; r_u = a! r''_u + S_u/a!; LSRK for u
       //      r''_p also goes to a zero-padded row copy (row stride N+1) in the dead face region for F
       {
@@ -1243,11 +1536,40 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
     }
 
     // ---- F-I: WADG multiply + telescoping projection of r_p
-    R osc[KO];
-    wadg_phases<C, R>(gb, q, A, sync, pt_prev, osc);
-    constexpr int RES = wadg_result<C>();
+    R osc[KO];  // TRIPLE: b_N at the lane's shell slots; v4: the output scales a!/N!
+    constexpr bool M0FAST = (M == 0) && BBW_M0_FAST;
+    if constexpr (M0FAST) {
+      // M = 0 (piecewise-constant c^2, BBDG): P^N_N = I (c_0 = 1, c_j = 0 for j >= 1), so the WADG
+      // update is the multiplication of r_p by the element's constant c^2: dp/dt_a = c^2 a! r''_p[a]; the
+      // product and the telescoping sweeps are skipped
+      const R c0 = ld<R>(gb + C::O_C * RB);
+#pragma unroll
+      for (int k = 0; k < KO; ++k) osc[k] = c0 * __ldg(facN + cmin(q + TG * k, NP - 1));
+    } else {
+      wadg_phases<C, R>(gb, q, A, sync, pt_prev, osc);
+    }
+    constexpr int RES = M0FAST ? C::O_RP : C::TRIPLE ? C::tlev(N) : wadg_result<C>();
+    // TRIPLE: shell index (layout.hpp) of the lane's canonical coefficients a = q + TG k, where J reads b_N
+    int cshk[KO];
+#pragma unroll
+    for (int k = 0; k < KO; ++k)
+      cshk[k] = (C::TRIPLE && !M0FAST)
+                    ? (int)__ldg(reinterpret_cast<const uint32_t*>(tab + L.sho) + cmin(q + TG * k, NP - 1))
+                    : q + TG * k;
 
     // ---- J: dp/dt = a!/N! b_N; outputs
+#if BBW_LSRK_TMEM
+    if (A.mode == 0) {
+      R t0[TMR], t1[TMR];
+      tm_load_reals<R, TMR>(taddr, 0, t0);
+      tm_load_reals<R, TMR>(taddr, TMW, t1);
+#pragma unroll
+      for (int i = 0; i < KO; ++i) {
+        rs[0][0][i] = t0[i];
+        qo[0][0][i] = t1[i];
+      }
+    }
+#endif
 #if BBW_LSRK_REG
 #define BBW_QP(u, k) qo[u][0][k]
 #define BBW_SP(u, k) rs[u][0][k]
@@ -1258,9 +1580,9 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
       for (int u = 0; u < ET; ++u)
 #pragma unroll
         for (int k = 0; k < KO; ++k) {
-          const int a = q + TG * k;
+          const int a = BBW_PA(k);
           const long long gi = (k0 + u) * 4 * NP + a;
-          const bool ok = u < nE && a < NP;
+          const bool ok = u < nE && q + TG * k < NP;
           qp[u][k] = ok ? __ldg(A.Qin + gi) : R(0);
           sp[u][k] = ok ? __ldcs(A.res + gi) : R(0);
         }
@@ -1270,14 +1592,14 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
 #endif
 #pragma unroll
     for (int k = 0; k < KO; ++k) {
-      const int a = q + TG * k;
-      if (a < NP) {
-        const R sc = osc[k];
+      const int a = BBW_PA(k);
+      if (q + TG * k < NP) {
+        const R sc = (C::TRIPLE && !M0FAST) ? __ldg(outN + a) : osc[k];  // a!/N! (M0FAST: c^2 a!)
 #pragma unroll
         for (int u = 0; u < ET; ++u) {
           if (u >= nE) continue;
           const long long kk = k0 + u;
-          const R dp = ld<R>(gb + u * EB + (RES + a) * RB) * sc;
+          const R dp = ld<R>(gb + u * EB + (RES + cshk[k]) * RB) * sc;
           if (A.mode == 2) {
             A.Qout[kk * NP + a] = dp;
           } else {
@@ -1299,20 +1621,32 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
     sync();
     BBW_PT(10);
   }
+#if BBW_LSRK_TMEM
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_s), "r"(TMCOLS) : "memory");
+#endif
 }
 
-// Halo pack: for each send face (local element k, face f) write the 4 own traces in the
-// sender's canonical face ordering: buf[slot][c][i] = Q[k][c][fnode[f][i]].
+// Halo pack: for each send face (local element k, face f) write the two traces the
+// receiver's flux needs (Eq. sdf), in the sender's canonical face ordering:
+//   buf[slot][0][i] = p(face node i),   buf[slot][1][i] = u(face node i) . n_f,
+// n_f = -grad(lambda_f)/|grad(lambda_f)| the sender's outward unit normal (2 Nfp words per face).
 template <int N, typename R>
-__global__ void pack_kernel(const R* __restrict__ Q, const int* __restrict__ faces, int nfaces,
-                            const uint16_t* __restrict__ fnode_bytes, R* __restrict__ buf) {
+__global__ void pack_kernel(const R* __restrict__ Q, const R* __restrict__ geo, const int* __restrict__ faces,
+                            int nfaces, const uint16_t* __restrict__ fnode_bytes, R* __restrict__ buf) {
   constexpr int NP = cnp3(N), NFP = cnp2(N);
-  const long long total = (long long)nfaces * 4 * NFP;
+  const long long total = (long long)nfaces * NFP;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int slot = (int)(t / (4 * NFP));
-    const int r = (int)(t - (long long)slot * 4 * NFP), c = r / NFP, i = r - c * NFP;
+    const int slot = (int)(t / NFP), i = (int)(t - (long long)slot * NFP);
     const int k = faces[2 * slot], f = faces[2 * slot + 1];
-    buf[t] = Q[(long long)k * 4 * NP + c * NP + __ldg(fnode_bytes + f * NFP + i) / (int)sizeof(R)];
+    const R* g = geo + (long long)k * 12 + 3 * f;
+    const R gx = g[0], gy = g[1], gz = g[2];
+    const R il = R(1) / sqrt(gx * gx + gy * gy + gz * gz);
+    const R* qk = Q + (long long)k * 4 * NP + __ldg(fnode_bytes + f * NFP + i) / (int)sizeof(R);
+    R* b = buf + (long long)slot * 2 * NFP + i;
+    b[0] = qk[0];
+    b[NFP] = (-gx * il) * qk[NP] + (-gy * il) * qk[2 * NP] + (-gz * il) * qk[3 * NP];
   }
 }
 

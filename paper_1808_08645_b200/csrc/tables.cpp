@@ -364,6 +364,33 @@ HostTables build_tables(int N, int M, int RB) {
       W.real(L.s_invf2, i, 1.0L / (f * f), RB);
     }
   }
+  // shell-order tables (layout.hpp)
+  {
+    auto fsh = [](int a1, int a2, int a3) {
+      const int d = a1 + a2 + a3;
+      return np3(d - 1) + a3 * (2 * d + 3 - a3) / 2 + a2;
+    };
+    const int nd = std::max(N + M - 1, N);  // SHD up to degree N+M-1; SHU/SHO/SHW/SHS up to degree N
+    for (int d = 0; d <= nd; ++d)
+      for (int a3 = 0; a3 <= d; ++a3)
+        for (int a2 = 0; a2 <= d - a3; ++a2) {
+          const int a1 = d - a2 - a3, f = fsh(a1, a2, a3);
+          const int f1 = fsh(a1 + 1, a2, a3);
+          if (fsh(a1, a2 + 1, a3) != f1 + 1 || fsh(a1, a2, a3 + 1) != f1 + d + 2 - a3 || f1 > 0xFFFF)
+            throw std::runtime_error("shell-order relation broken");
+          W.put<uint32_t>(L.shd, f, (uint32_t)f1 | ((uint32_t)(d + 2 - a3) << 16));
+          if (d <= N) {
+            const int u1 = a1 > 0 ? fsh(a1 - 1, a2, a3) + 1 : 0, u2 = a2 > 0 ? fsh(a1, a2 - 1, a3) + 1 : 0,
+                      u3 = a3 > 0 ? fsh(a1, a2, a3 - 1) + 1 : 0;
+            if (u1 > 255 || u2 > 255 || u3 > 255) throw std::runtime_error("shell up offset overflow");
+            W.put<uint32_t>(L.shu, f, (uint32_t)u1 | ((uint32_t)u2 << 8) | ((uint32_t)u3 << 16) | ((uint32_t)d << 24));
+            W.put<uint32_t>(L.sho, rank3(N, a1, a2, a3), (uint32_t)f);  // canonical a -> shell index
+            const long double g = lfact(a1) * lfact(a2) * lfact(a3);
+            W.real(L.shw, f, 1.0L / (g * g), RB);
+            W.real(L.shs, f, g * lfact(N - d) / lfact(N), RB);
+          }
+        }
+  }
   auto c = projection_constants(N, M);
   for (int j = 0; j <= N; ++j) {
     T.cj[j] = c[j];

@@ -27,7 +27,8 @@ class bbwadg_options(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("tau_p", ctypes.c_double), ("tau_u", ctypes.c_double),
                 ("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world_size", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
-                ("partition", ctypes.c_int * 3), ("check_c2", ctypes.c_int), ("reserved", ctypes.c_int * 7)]
+                ("partition", ctypes.c_int * 3), ("check_c2", ctypes.c_int), ("reserved0", ctypes.c_int),
+                ("c2_gids", ctypes.c_void_p), ("c2_rows", ctypes.c_int64), ("reserved", ctypes.c_int * 4)]
 
 
 class bbwadg_info(ctypes.Structure):

@@ -20,7 +20,7 @@ from . import lib as L
 class Solver:
     def __init__(self, vertices, elements, N: int, M: int, c2, *, dtype: str = "f64", tau_p: float = 1.0,
                  tau_u: float = 1.0, device: int = 0, stream=None, rank: int = 0, world_size: int = 1,
-                 nccl_id: bytes | None = None, partition=None, check_c2: bool = True):
+                 nccl_id: bytes | None = None, partition=None, check_c2: bool = True, c2_gids=None):
         import torch
 
         self.torch = torch
@@ -32,7 +32,12 @@ class Solver:
         self._v = np.ascontiguousarray(vertices, dtype=np.float64)
         self._e = np.ascontiguousarray(elements, dtype=np.int64)
         c2 = np.ascontiguousarray(c2, dtype=np.float64)
-        if c2.shape != (self._e.shape[0], self.Mp):
+        self._c2_gids = None
+        if c2_gids is not None:  # rows for these global ids only (e.g. this rank's partition)
+            self._c2_gids = np.ascontiguousarray(c2_gids, dtype=np.int64)
+            if c2.shape != (self._c2_gids.shape[0], self.Mp):
+                raise ValueError(f"c2 must have shape [len(c2_gids), {self.Mp}]")
+        elif c2.shape != (self._e.shape[0], self.Mp):
             raise ValueError(f"c2 must have shape [K, {self.Mp}]")
         o = L.bbwadg_default_options()
         o.dtype = L.BBWADG_F64 if dtype == "f64" else L.BBWADG_F32
@@ -53,6 +58,9 @@ class Solver:
             for i in range(3):
                 o.partition[i] = int(partition[i])
         o.check_c2 = 1 if check_c2 else 0
+        if self._c2_gids is not None:
+            o.c2_gids = self._c2_gids.ctypes.data
+            o.c2_rows = int(self._c2_gids.shape[0])
         self.ctx = L.bbwadg_setup(self._v, self._e, self.N, self.M, c2, o)
         info = self.info()
         self.K_local = info["num_elements_local"]

@@ -62,8 +62,27 @@ def main():
     ap.add_argument("--n", type=int, nargs="+", default=[4, 8, 16])
     ap.add_argument("--T", type=float, default=0.5)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--study", choices=["refinement", "wavespeed"], default="refinement")
+    ap.add_argument("--study", choices=["refinement", "wavespeed", "mlessn"], default="refinement")
     a = ap.parse_args()
+    if a.study == "mlessn":
+        # P:678 / Fig. con3d: N = 4 and 5, M = 0, 1, 2 < N; observed rate r = 2 for M = 0 and
+        # r = min(N+1, M+3) for M >= 1 (4 for M = 1, 5 for N = 4 / M = 2); smooth c^2 (k = 1) as in the paper
+        rows = []
+        for N in (4, 5):
+            for M in (0, 1, 2):
+                prev = None
+                for n in a.n:
+                    r = run_case(N, n, a.T, M=M)
+                    r["rate"] = None if prev is None else float(np.log2(prev / r["err_p"]))
+                    r["predicted_rate"] = 2 if M == 0 else min(N + 1, M + 3)
+                    prev = r["err_p"]
+                    rows.append(r)
+                    print(json.dumps(r), flush=True)
+        out = {"study": "P:678 M < N convergence (3D): N = 4, 5; M = 0, 1, 2; Kuhn meshes n = %s, T = %g" % (a.n, a.T),
+               "predicted_rate": "2 for M = 0, min(N+1, M+3) for M >= 1 (P:678)", "rows": rows}
+        with open(a.out or os.path.join(ROOT, "profiles", "convergence_mlessn_r2.json"), "w") as fh:
+            json.dump(out, fh, indent=1)
+        return
     if a.study == "wavespeed":
         # P:1048-1251 (Fig. wavespeed, 3D): N = 6, uniform mesh h = 0.0833 (n = 24 cubes on [-1,1]^3,
         # 82,944 tets), c^2 = 1 + 1/2 sin(k pi x) sin(k pi y) sin(k pi z), k = 1, 4, 8, 12, M = 0..N;

@@ -16,7 +16,8 @@ sys.path.insert(0, HERE)
 import ncu_lines  # noqa: E402
 
 MARK = [(r"__forceinline__ void sum4_phase", "sum4 (G,H)"), (r"__forceinline__ void face_sum3", "face_sum3 (C2,D)"),
-        (r"__forceinline__ void zero_pad_rows", "zero_pad_rows"), (r"// F: h'_g", "F product"),
+        (r"__forceinline__ void zero_pad_rows", "zero_pad_rows"), (r"// F: h'_g", "F product"), (r"// F \(v5\)", "F product"),
+        (r"auto reduce = \[&\]", "G/H tri reduce"), (r"// I: upward, in place", "I upward"),
         (r"// G: M reductions", "G call"), (r"// H: downward", "H call"), (r"// I: upward", "I upward"),
         (r"void __launch_bounds__", "kernel prologue"), (r"// ---- A:", "A loads"), (r"// ---- B1", "B1 flux"),
         (r"// ---- B2", "B2 grad"), (r"// ---- C1", "C1 vol elev"), (r"// ---- C2", "C2"), (r"// ---- C3", "C3 L0"),

@@ -118,7 +118,14 @@ def test_setup_without_device_fails_loudly(L):
 
 
 def test_setup_validates_arguments_before_device(L):
+    # host-side validation runs before the device query, so these fail with their own status even
+    # on a machine without a GPU (status names, not just "an error")
     v = np.zeros((4, 3))
     e = np.array([[0, 1, 2, 3]], dtype=np.int64)
-    with pytest.raises(L.BBWADGError):
+    with pytest.raises(L.BBWADGError, match="MESH"):  # degenerate tet: J = 0
         L.bbwadg_setup(v, e, 3, 1, np.ones((1, 4)), L.bbwadg_default_options())
+    v = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    with pytest.raises(L.BBWADGError, match="UNSUPPORTED"):  # N > 9
+        L.bbwadg_setup(v, e, 10, 1, np.ones((1, 4)), L.bbwadg_default_options())
+    with pytest.raises(L.BBWADGError, match="UNSUPPORTED"):  # M > N
+        L.bbwadg_setup(v, e, 2, 3, np.ones((1, 20)), L.bbwadg_default_options())

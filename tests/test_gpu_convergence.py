@@ -13,10 +13,10 @@ from workloads import errors, kuhn, media, states
 pytestmark = pytest.mark.gpu
 
 
-def _gpu_error(N, n, T=0.5):
+def _gpu_error(N, n, T=0.5, M=None):
     from paper_1808_08645_b200 import Solver
 
-    M = N
+    M = N if M is None else M
     v, e = kuhn.kuhn_mesh(n)
     f = media.c2_smooth(1.0)
     c2 = media.project_c2(v, e, f, M)
@@ -66,3 +66,13 @@ def test_gpu_error_equals_oracle_error(gpu_lib):
     eg = errors.l2_error(v, e, Qg[:, 0], N, ex)
     assert abs(eo - eg) <= 1e-9 * eo, (eo, eg)
     assert abs(eo - o.l2_error(Qo, states.manufactured_exact, T, q=N + 4)) <= 1e-12 * eo  # same rule, same norm
+
+
+@pytest.mark.parametrize("N,M,rmin", [(4, 0, 1.6), (4, 1, 3.4), (5, 1, 3.4)])
+def test_convergence_rate_M_below_N(gpu_lib, N, M, rmin):
+    # r = 2 for M = 0 and min(N+1, M+3) for M >= 1 (M = 1: 4), between n = 8 and n = 16
+    # (3,072 -> 24,576 tets; the paper's coarsest step is pre-asymptotic for M = 0 as well)
+    e8, e16 = _gpu_error(N, 8, M=M), _gpu_error(N, 16, M=M)
+    rate = np.log2(e8 / e16)
+    predicted = 2 if M == 0 else min(N + 1, M + 3)
+    assert rmin < rate < predicted + 0.8, (N, M, e8, e16, rate)

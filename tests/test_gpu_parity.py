@@ -235,9 +235,12 @@ def test_nonfinite_detection(gpu_lib):
 
 # ------------------------------------------------------------------------------------ partitions
 @pytest.mark.parametrize("nparts,N,M", [(2, 4, 2), (4, 4, 2), (8, 4, 2), (4, 7, 4), (8, 2, 1)])
-def test_group_partition_bitwise(gpu_lib, nparts, N, M):
-    """P in-process partitions with device-copy halos == 1 partition, bitwise; N = 2, 4 run
-    sub-warp element groups over the interior / boundary element ranges of each partition."""
+def test_group_partition_matches_single(gpu_lib, nparts, N, M):
+    """P in-process partitions with device-copy halos == 1 partition; N = 2, 4 run sub-warp
+    element groups over the interior / boundary element ranges of each partition.  The halo carries p and
+    u.n_sender only (Eq. sdf), so a partition face forms n.[[u]] as -u+.n+ - n.u- instead of
+    n.(u+ - u-): equal up to rounding (n+ = -n up to fp64 rounding), not bitwise; every element is within
+    1e-13 (per-element max, relative to the state's max) of the single-partition run."""
     from paper_1808_08645_b200 import lib as L
 
     v, e = kuhn.kuhn_mesh(4)
@@ -267,7 +270,8 @@ def test_group_partition_bitwise(gpu_lib, nparts, N, M):
         out[g] = loc
     for c in ctxs:
         L.bbwadg_destroy(c)
-    assert np.array_equal(out, ref)
+    per_elem = np.max(np.abs(out - ref), axis=(1, 2)) / np.max(np.abs(ref))
+    assert per_elem.max() <= 1e-13, per_elem.max()
 
 
 # ------------------------------------------------------------------------------------ full sizes

@@ -466,3 +466,36 @@ def test_oracle_step_uses_stage_times():
         res = float(LSRK_A[s]) * res + dt * o.rhs(q2, t0 + cs * dt)
         q2 = q2 + float(LSRK_B[s]) * res
     assert np.max(np.abs(q2 - q)) > 1e-12 * np.max(np.abs(q))
+
+
+# --------------------------------------------------------------------------- diagnostics
+def test_energy_with_constant_wavespeed_is_plain_l2():
+    # R22 / P:136-137: for constant c^2 the WADG norm p^T M M_{c^2}^-1 M p reduces to int p^2 / c^2, so
+    # E = 1/2 sum_k [int p^2 / c^2 + int |u|^2], computed here by an independent quadrature (workloads'
+    # Stroud rule, exact to 2N+7) of the evaluated fields
+    from workloads.errors import l2_error
+
+    N, M, cval = 3, 0, 1.7
+    v, e = kuhn.kuhn_mesh(2)
+    c2 = np.full((len(e), 1), cval)
+    o = AcousticOracle(v, e, N, M, c2)
+    Q = np.random.default_rng(5).standard_normal((len(e), 4, bb.num_coeffs(N)))
+    zero = lambda x, y, z: 0.0 * x  # noqa: E731
+    ip = l2_error(v, e, Q[:, 0], N, zero) ** 2
+    iu = sum(l2_error(v, e, Q[:, c], N, zero) ** 2 for c in (1, 2, 3))
+    ref = 0.5 * (ip / cval + iu)
+    assert abs(o.energy(Q) - ref) <= 1e-12 * ref
+
+
+def test_oracle_l2_error_matches_independent_quadrature():
+    # the oracle's error norm (R18) against workloads.errors (its own rule and basis evaluation)
+    from workloads.errors import l2_error
+
+    N = 3
+    v, e = kuhn.kuhn_mesh(2)
+    o = AcousticOracle(v, e, N, 1, media.random_c2(len(e), 1))
+    Q = np.random.default_rng(6).standard_normal((len(e), 4, bb.num_coeffs(N)))
+    f = lambda x, y, z, t: (np.sin(x + 2 * y) * np.cos(z - t), 0, 0, 0)  # noqa: E731
+    a = o.l2_error(Q, f, 0.3, q=N + 6)
+    b = l2_error(v, e, Q[:, 0], N, lambda x, y, z: f(x, y, z, 0.3)[0], q=N + 6)
+    assert abs(a - b) <= 1e-12 * b
