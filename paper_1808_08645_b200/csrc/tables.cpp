@@ -137,14 +137,24 @@ std::vector<std::pair<int, int>> product_row_order_uncached(int N, int M, int RB
       const int lamax = std::min(N + 1, N + 1 - smin + Bs[b].first + Bs[b].second);
       nvec[b] = anyv[b] ? (lamax + VEC - 1) / VEC : 0;
     }
+    // product v5 (stage_kernel.cuh): a lane loads only the vectors of ITS input row that exist (predicated
+    // on its own row length), invalid lanes load nothing
+    auto lenA = [&](int r, int b) {
+      if (r < 0) return 0;
+      const int a2 = G[r].first - Bs[b].first, a3 = G[r].second - Bs[b].second;
+      return (a2 >= 0 && a3 >= 0 && a2 + a3 <= N) ? N + 1 - a2 - a3 : 0;
+    };
     auto qcost = [&](int q0) {  // loads of lanes q0..q0+7 over every c''-row and vector
-      int c = 0, ad[8];
+      int c = 0, ad[8], ln[8];
       for (int b = 0; b < NB; ++b) {
         if (!nvec[b]) continue;
-        for (int l = 0; l < 8; ++l) ad[l] = unit(rr[q0 + l], b);
+        for (int l = 0; l < 8; ++l) {
+          ad[l] = unit(rr[q0 + l], b);
+          ln[l] = lenA(rr[q0 + l], b);
+        }
         for (int v = 0; v < nvec[b]; ++v) {
           int av[8];
-          for (int l = 0; l < 8; ++l) av[l] = ad[l] < 0 ? -1 : ad[l] + v;
+          for (int l = 0; l < 8; ++l) av[l] = (ad[l] < 0 || VEC * v >= ln[l]) ? -1 : ad[l] + v;
           c += group_cost(av, 8, 8);
         }
       }
