@@ -165,6 +165,25 @@ const char* bbwadg_error_string(bbwadg_ctx ctx);
 const char* bbwadg_last_error(void);
 void bbwadg_destroy(bbwadg_ctx ctx);
 
+/* ---- elastic BBWADG: velocity-stress elastic wave equation, Eq. ewave
+ * (P:150-157), DG form with penalty fluxes P:198-206, matrix-weighted WADG update Eq. ewadg
+ * with the isotropic C of P:185-195.  One fused kernel per RK stage (volume, surface, ten scalar
+ * weight-adjusted applications, LSRK); R25-R28.
+ *   rho_inv, lambda, mu: host [K][Mp] degree-M Bernstein coefficients of rho^-1 and the Lame
+ *              parameters per element (global order); setup rejects rho^-1 <= 0, lambda + 2 mu <= 0
+ *              or mu < 0 at the check points (opts->check_c2).
+ *   opts:      tau_p is the stress penalty tau_sigma, tau_u the velocity penalty tau_v (the acoustic
+ *              p <-> sigma, u <-> v correspondence); world_size must be 1; c2_gids unused.
+ * The returned context uses the common calls with 9 fields: state Q[K][9][Np] with fields
+ * (v_1, v_2, v_3, s11, s22, s33, s23, s13, s12) (Voigt order of the A_i rows);
+ * bbwadg_rhs gives dQ/dt of Eq. ewadg; bbwadg_wadg_apply maps r[K][9][Np] to
+ * (P_N(rho^-1 r_v), (I x M^-1) M_C r_sigma); step/run/get/set_state/query/destroy as above;
+ * bbwadg_set_source and partition groups are not available (BBWADG_ERR_UNSUPPORTED /
+ * BBWADG_ERR_INVALID_ARG).  Errors as for bbwadg_setup. */
+bbwadg_status bbwadg_elastic_setup(const bbwadg_mesh* mesh, int N, int M, const double* rho_inv,
+                                   const double* lambda, const double* mu, const bbwadg_options* opts,
+                                   bbwadg_ctx* out);
+
 /* ---- in-process partition groups (test/debug: P partitions on one device,
  * halo exchanged by device copies instead of NCCL; validates partitioning,
  * packing, orientation and the interior/boundary split without a cluster) */

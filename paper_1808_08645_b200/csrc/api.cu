@@ -15,6 +15,7 @@
 #include "dispatch.hpp"
 #include "mesh.hpp"
 #include "nccl_shim.hpp"
+#include "elastic_kernel.cuh"
 #include "stage_kernel.cuh"
 #include "tables.hpp"
 #include "layout.hpp"
@@ -53,6 +54,8 @@ struct Group;
 
 struct bbwadg_ctx_s {
   int N = 0, M = 0, dtype = 0, device = 0, Np = 0, Mp = 0, Nfp = 0;
+  int nfields = 4;       // 4 acoustic (p, u), 9 elastic (v, sigma)
+  bool elastic = false;  // bbwadg_elastic_setup context (NEXT-2)
   size_t rb = 8;  // bytes per real
   double tau_p = 1, tau_u = 1;
   cudaStream_t stream = nullptr;
@@ -130,10 +133,43 @@ void fill_args(bbwadg_ctx c, StageArgs<R>& a) {
   }
 }
 
+// Elastic stage kernel over local elements [b, e) (Qin/Qout/res: [K][9][Np]).
+template <typename R>
+bbwadg_status launch_elastic_typed(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e,
+                                   double rk_a, double rk_b, double dt, int grid) {
+  ElasticArgs<R> a;
+  std::memset(&a, 0, sizeof(a));
+  fill_args(c, a.s);
+  a.s.Qin = static_cast<const R*>(Qin);
+  a.s.Qout = static_cast<R*>(Qout);
+  a.s.res = static_cast<R*>(c->d_res);
+  a.s.elem_begin = b;
+  a.s.elem_end = e;
+  a.s.rk_a = (R)rk_a;
+  a.s.rk_b = (R)rk_b;
+  a.s.dt = (R)dt;
+  a.s.mode = mode;
+  a.mat = static_cast<const R*>(c->d_c2);
+  a.tau_s = (R)c->tau_p;  // elastic contexts: tau_p carries tau_sigma, tau_u carries tau_v (header)
+  a.tau_v = (R)c->tau_u;
+  cudaError_t err = c->ks.launch_elastic(&a, grid, c->stream);
+  if (err != cudaSuccess) return fail(c, BBWADG_ERR_CUDA, std::string("elastic kernel launch: ") + cudaGetErrorString(err));
+  return BBWADG_OK;
+}
+
+bbwadg_status launch_elastic_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e,
+                                  double rk_a, double rk_b, double dt) {
+  const int64_t nb = (e - b + c->ks.elastic_elems_per_cta - 1) / c->ks.elastic_elems_per_cta;
+  const int grid = (int)std::min<int64_t>(nb, c->grid);
+  return c->dtype == BBWADG_F64 ? launch_elastic_typed<double>(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt, grid)
+                                : launch_elastic_typed<float>(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt, grid);
+}
+
 // Launch one kernel pass over local elements [b, e).
 bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e, double rk_a,
                           double rk_b, double dt, double tstage, int grid_cap = 0) {
   if (e <= b) return BBWADG_OK;
+  if (c->elastic) return launch_elastic_pass(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt);
   int64_t nb = (e - b + c->ks.elems_per_cta - 1) / c->ks.elems_per_cta;
   int grid = (int)std::min<int64_t>(nb, grid_cap > 0 ? grid_cap : c->grid);
   cudaError_t err;
@@ -232,7 +268,7 @@ bbwadg_status full_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, dou
   return launch_pass(c, mode, Qin, Qout, 0, P.K_local, rk_a, rk_b, dt, tstage);
 }
 
-size_t state_bytes(bbwadg_ctx c) { return (size_t)c->part.K_local * 4 * c->Np * c->rb; }
+size_t state_bytes(bbwadg_ctx c) { return (size_t)c->part.K_local * c->nfields * c->Np * c->rb; }
 
 template <typename R>
 __global__ void nonfinite_kernel(const R* __restrict__ q, long long n, int* flag) {
@@ -297,8 +333,9 @@ struct C2Checker {
   }
 };
 
+// c2: acoustic [rows][Mp] c^2_M; elastic (elastic = true) [K][3][Mp] (rho^-1, lambda, mu) interleaved per element
 bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, const bbwadg_options& o, int rank,
-                        int nparts, cudaStream_t shared_stream, bbwadg_ctx* out) {
+                        int nparts, cudaStream_t shared_stream, bbwadg_ctx* out, bool elastic = false) {
   std::unique_ptr<bbwadg_ctx_s> c(new bbwadg_ctx_s());
   struct Cleanup {  // release device resources on every early-error return
     std::unique_ptr<bbwadg_ctx_s>& p;
@@ -317,13 +354,17 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   c->Mp = np3(M);
   c->Nfp = np2(N);
   c->K_global = g.K;
+  c->elastic = elastic;
+  c->nfields = elastic ? 9 : 4;
   CUDA_TRY(c.get(), cudaSetDevice(o.device));
   c->ks = get_kernels(N, M, o.dtype);
-  if (!c->ks.launch_stage) return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "no kernel instantiation for this (N, M, dtype)");
+  if (!c->ks.launch_stage || (elastic && !c->ks.launch_elastic))
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "no kernel instantiation for this (N, M, dtype)");
   CUDA_TRY(c.get(), c->ks.prepare());
+  if (elastic) CUDA_TRY(c.get(), c->ks.prepare_elastic());
   int nsm = 0;
   CUDA_TRY(c.get(), cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
-  c->grid = nsm * c->ks.blocks_per_sm();
+  c->grid = nsm * (elastic ? c->ks.elastic_blocks_per_sm() : c->ks.blocks_per_sm());
   if (const char* e = getenv("BBWADG_BLOCKS_PER_SM")) {  // tuning: occupancy sensitivity experiments
     const int b = atoi(e);
     if (b > 0 && b < c->ks.blocks_per_sm()) c->grid = nsm * b;
@@ -344,7 +385,8 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   CUDA_TRY(c.get(), cudaMemcpy(c->d_tab, c->tables.blob.data(), c->tables.blob.size(), cudaMemcpyHostToDevice));
   // per-element inputs in local order
   const int64_t KL = P.K_local;
-  std::vector<double> geo(12 * KL), c2l((size_t)KL * c->Mp);
+  const int W = elastic ? 3 * c->Mp : c->Mp;  // material reals per element
+  std::vector<double> geo(12 * KL), c2l((size_t)KL * W);
   // c^2 rows: global order, or only the listed global ids (o.c2_gids, sorted lookup)
   std::vector<std::pair<int64_t, int64_t>> c2map;
   if (o.c2_gids) {
@@ -372,9 +414,24 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
 #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < KL; ++i) {
     element_gradients(g, P.gid[i], &geo[12 * i]);
-    const double* ci = c2 + (size_t)c2row[i] * c->Mp;
-    std::memcpy(&c2l[(size_t)i * c->Mp], ci, sizeof(double) * c->Mp);
-    if (o.check_c2) {
+    const double* ci = c2 + (size_t)c2row[i] * W;
+    std::memcpy(&c2l[(size_t)i * W], ci, sizeof(double) * W);
+    if (o.check_c2 && elastic) {
+      // rho^-1 > 0, lambda + 2 mu > 0 (P-wave modulus), mu >= 0 at the sample points (R25; mu = 0 is the
+      // acoustic limit)
+      std::vector<double> pm(c->Mp);
+      for (int b = 0; b < c->Mp; ++b) pm[b] = ci[c->Mp + b] + 2.0 * ci[2 * c->Mp + b];
+      const double m0 = chk.min_value(ci), m1 = chk.min_value(pm.data()), m2 = chk.min_value(ci + 2 * c->Mp);
+      if (!(m0 > 0) || !(m1 > 0) || !(m2 >= 0)) {
+#pragma omp critical
+        {
+          if (bad < 0 || P.gid[i] < bad) {
+            bad = P.gid[i];
+            badv = std::min(m0, std::min(m1, m2));
+          }
+        }
+      }
+    } else if (o.check_c2) {
       // convex hull property: all Bernstein coefficients > 0 => c^2_M > 0 on the element
       bool allpos = true;
       for (int b = 0; b < c->Mp; ++b) allpos = allpos && (ci[b] > 0);
@@ -392,7 +449,8 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   }
   if (bad >= 0) {
     std::ostringstream os;
-    os << "c^2_M is not positive in element " << bad << " (sampled value " << badv << ")";
+    os << (elastic ? "rho^-1 / lambda + 2 mu / mu" : "c^2_M") << " is not positive in element " << bad
+       << " (sampled value " << badv << ")";
     return fail(nullptr, BBWADG_ERR_NONPOSITIVE_C2, os.str());
   }
   bbwadg_status s;
@@ -507,6 +565,33 @@ bbwadg_status bbwadg_setup(const bbwadg_mesh* mesh, int N, int M, const double* 
   return BBWADG_OK;
 }
 
+bbwadg_status bbwadg_elastic_setup(const bbwadg_mesh* mesh, int N, int M, const double* rho_inv,
+                                   const double* lambda, const double* mu, const bbwadg_options* opts,
+                                   bbwadg_ctx* out) {
+  if (!out) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!rho_inv || !lambda || !mu) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "material pointers must not be NULL");
+  bbwadg_options o;
+  bbwadg_default_options(&o);
+  if (opts) o = *opts;
+  if (o.world_size != 1 || o.rank != 0)
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "elastic contexts run on one GPU (world_size 1)");
+  if (o.c2_gids) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "c2_gids is not used by elastic contexts");
+  GlobalMesh g;
+  bbwadg_status s = prepare_global(mesh, N, M, rho_inv, &o, 1, g);
+  if (s) return s;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(nullptr, BBWADG_ERR_NO_DEVICE, "no CUDA device");
+  const int Mp = np3(M);
+  std::vector<double> mat((size_t)g.K * 3 * Mp);
+  for (int64_t k = 0; k < g.K; ++k) {
+    std::memcpy(&mat[(size_t)k * 3 * Mp], rho_inv + (size_t)k * Mp, sizeof(double) * Mp);
+    std::memcpy(&mat[(size_t)k * 3 * Mp + Mp], lambda + (size_t)k * Mp, sizeof(double) * Mp);
+    std::memcpy(&mat[(size_t)k * 3 * Mp + 2 * Mp], mu + (size_t)k * Mp, sizeof(double) * Mp);
+  }
+  return setup_one(g, N, M, mat.data(), o, 0, 1, nullptr, out, true);
+}
+
 bbwadg_status bbwadg_setup_group(const bbwadg_mesh* mesh, int N, int M, const double* c2_coeffs,
                                  const bbwadg_options* opts, int nparts, bbwadg_ctx* out) {
   if (!out || nparts < 1) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad group arguments");
@@ -566,6 +651,7 @@ bbwadg_status bbwadg_get_state(bbwadg_ctx c, void* Q, int on_device) {
 
 bbwadg_status bbwadg_set_source(bbwadg_ctx c, const double* gsrc) {
   if (!c) return fail(c, BBWADG_ERR_INVALID_ARG, "null ctx");
+  if (c->elastic) return fail(c, BBWADG_ERR_UNSUPPORTED, "the manufactured source is acoustic only");
   CUDA_TRY(c, cudaSetDevice(c->device));
   if (c->d_src) {
     CUDA_TRY(c, cudaFree(c->d_src));
@@ -710,7 +796,8 @@ bbwadg_status bbwadg_query(bbwadg_ctx c, bbwadg_info* info) {
   info->global_ids = P.gid.data();
   // minimum HBM traffic of one fused stage: Q_in, res (read) + Q_out, res (write) = 16 Np words,
   // c^2_M (Mp words), geometry (12 words), connectivity (4 int32 + 4 bytes) per element.
-  const double per_elem = (16.0 * c->Np + c->Mp + 12.0) * c->rb + 20.0;
+  const double per_elem = c->elastic ? (36.0 * c->Np + 3.0 * c->Mp + 12.0) * c->rb + 20.0
+                                     : (16.0 * c->Np + c->Mp + 12.0) * c->rb + 20.0;
   info->algorithmic_bytes_per_stage = per_elem * P.K_local;
   const int N = c->N, M = c->M, Np = c->Np, Nfp = c->Nfp;
   double vol = 24.0 * np3(N - 1) + 8.0 * Np * 4;                  // gradient (24 flop/b) + elevation (8 flop/out)
@@ -720,6 +807,15 @@ bbwadg_status bbwadg_query(bbwadg_ctx c, bbwadg_info* info) {
   for (int n = N + 1; n <= N + M; ++n) proj += 8.0 * np3(n - 1);
   for (int n = 1; n <= N; ++n) proj += 8.0 * np3(n - 1) + 10.0 * np3(n);
   double lsrk = 4.0 * 4 * Np;
+  if (c->elastic) {
+    // 9-field gradient (144 flop per degree-(N-1) coefficient) + 9 elevations; fluxes (~90 flop per face
+    // node) + three 8-array lifts; ten scalar WADG applications; LSRK on 9 fields
+    vol = 144.0 * np3(N - 1) + 9.0 * 4 * Np;
+    surf = 4.0 * Nfp * 90.0 + 3.0 * (surf - 4.0 * Nfp * 20.0);
+    mult *= 10.0;
+    proj *= 10.0;
+    lsrk = 4.0 * 9 * Np;
+  }
   info->flops_per_stage = (vol + surf + mult + proj + lsrk) * P.K_local;
   info->kernels_per_stage = (P.nparts > 1) ? 3 : 1;
   info->steps_taken = c->steps;
@@ -855,6 +951,6 @@ int bbwadg_debug_phase_times(bbwadg_ctx c, unsigned long long* out) {
   return 0;
 }
 
-const char* bbwadg_version(void) { return "bbwadg-b200 0.1 (sm_100a, fused stage kernel v4)"; }
+const char* bbwadg_version(void) { return "bbwadg-b200 0.2 (sm_100a, fused acoustic stage kernel v5, elastic stage kernel e1)"; }
 
 }  // extern "C"

@@ -14,6 +14,11 @@ struct KernelSet {
   cudaError_t (*prepare)() = nullptr;  // set smem attributes
   int (*blocks_per_sm)() = nullptr;
   int smem_bytes = 0, elems_per_cta = 0, threads = 0;
+  // elastic stage kernel (NEXT-2); args points to ElasticArgs<double> / ElasticArgs<float>
+  cudaError_t (*launch_elastic)(const void* args, int grid, cudaStream_t s) = nullptr;
+  cudaError_t (*prepare_elastic)() = nullptr;
+  int (*elastic_blocks_per_sm)() = nullptr;
+  int elastic_smem_bytes = 0, elastic_elems_per_cta = 0, elastic_threads = 0;
 };
 
 KernelSet get_kernels(int N, int M, int dtype);

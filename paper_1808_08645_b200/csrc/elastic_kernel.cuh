@@ -1,0 +1,412 @@
+// Fused elastic BBWADG RK-stage kernel for sm_100a (DESIGN.md §6 "elastic").
+//
+// Velocity-stress elastic wave equation, Eq. ewave, DG form P:198-206, matrix-weighted WADG
+// update Eq. ewadg.  Per element and RK stage, fields (v1, v2, v3, s11, s22, s33, s23, s13, s12)
+// (R25):
+//   volume   r_v = sum_i A_i^T d_i sigma, r_sigma = sum_i A_i d_i v (sparse barycentric derivative at degree
+//            N-1 for the 9 combinations, then degree elevation; factorial-scaled sums as in stage_kernel)
+//   surface  per face: [[v]], [[sigma]] (traction-free mirror on the boundary, R26), [[t]] = A_n^T [[sigma]],
+//            F_v = 1/2 [[t]] + tau_v/2 A_n^T A_n [[v]],  w = 1/2 [[v]] + tau_s/2 [[t]]  (F_sigma = A_n w);
+//            the 24 face arrays are lifted in three batches of eight (F_v[b], w[b] for the 4 faces, the
+//            acoustic (F_p, F_u) pair structure), each by L_0 and the N face-reduction layers;
+//            r_v[b] += sum_f lift_f(F_v[b]), r_sigma += sum_f A_n(f)[:, b] lift_f(w[b])
+//   WADG     ten scalar weight-adjusted applications P_N(w r) (Bernstein product Eq. mcoeff P:342-345 +
+//            telescoping projection Eq. telescope, stage_kernel's wadg_phases): rho^-1 on the three
+//            velocities, lambda on s = r_s11 + r_s22 + r_s33, mu on the six stresses, then
+//            dv = W_rho(r_v), ds_i = W_lambda(s) + 2 W_mu(r_si) (i < 3), W_mu(r_si) (i >= 3)
+//            (linearity of the projection: the paper's "process fewer components at a time", P:1523-1525,
+//            one component per application, so only one degree-(N+M) product is live per element)
+//   LSRK     res = a_s res + dt rhs; Q_out = Q_in + b_s res, state in registers.
+// The element block starts with the acoustic StageCfg layout (GEO, C, RP, then the WADG work region), so
+// wadg_phases<StageCfg> runs unchanged on it; the elastic volume/surface arrays overlay that region.
+#pragma once
+#include "stage_kernel.cuh"
+
+namespace bbw {
+
+__host__ __device__ constexpr int elastic_threads(int tg) { return tg <= 32 ? 64 : 128; }
+
+template <int N_, int M_, typename R>
+struct ElasticCfg {
+  using AC = StageCfg<N_, M_, R>;
+  static constexpr int N = N_, M = M_;
+  static constexpr int NP = AC::NP, NFP = AC::NFP, NFP1 = AC::NFP1, MP = AC::MP, NPM1 = AC::NPM1;
+  static constexpr int RB = AC::RB, VEC = AC::VEC, TG = AC::TG, KO = AC::KO, ET = 1;
+  static constexpr int T = elastic_threads(TG);
+  static constexpr int G = T / TG, GPW = TG < 32 ? 32 / TG : 1;
+  // per-element layout (reals): the acoustic block [0, AC::PER_E) (GEO at 0, c'' of the current WADG
+  // application at AC::O_C, WADG work region from AC::O_X), with the elastic volume/surface arrays
+  // overlaying [O_X, ...) and the three material arrays after everything
+  static constexpr int O_GEO = 0, O_X = AC::O_X;
+  static constexpr int EQ = O_X;                     // Q_in, 9 NP (volume / surface phases)
+  static constexpr int EG = EQ + 9 * NP;             // 9 gradient arrays, each (zero slot + NPM1)
+  static constexpr int EF = EQ + 9 * NP;             // fluxes [3 batches][4 faces][2][NFP] (G dead)
+  static constexpr int EY = EF + 24 * NFP;           // Y'' [8][NFP1 + 1]
+  static constexpr int EL = rup(EY + 8 * (NFP1 + 1), VEC);  // lift layers [8][NP]
+  static constexpr int EVS_END = cmax(EG + 9 * (NPM1 + 1), EL + 8 * NP);
+  static constexpr int ECM = rup(cmax(EVS_END, AC::PER_E), VEC);  // rho^-1'', lambda'', mu'' [3][MP]
+  static constexpr int PER_E = rup(ECM + 3 * MP, VEC);
+  static constexpr int EB = PER_E * RB;
+  static constexpr int GB = EB;
+  static constexpr int SMEM_BYTES = G * GB + 8 * G;
+  // resident CTAs per SM allowed by shared memory (227 KB per SM usable): caps registers per thread
+  static constexpr int MINB = cmax(1, cmin(8, (227 * 1024) / SMEM_BYTES));
+  static_assert(SMEM_BYTES <= 227 * 1024, "elastic element block exceeds shared memory");
+};
+
+template <typename R>
+struct ElasticArgs {
+  StageArgs<R> s;      // tab, gam, rk_a, rk_b, dt, mode, elem range (Qin/Qout/res: [K][9][NP])
+  const R* mat;        // [K][3][MP]: rho^-1, lambda, mu (degree-M Bernstein coefficients)
+  R tau_v, tau_s;
+};
+
+template <class EC, typename R>
+__global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const ElasticArgs<R> EA) {
+  using AC = typename EC::AC;
+  constexpr int N = EC::N, M = EC::M, NP = EC::NP, NFP = EC::NFP, NFP1 = EC::NFP1, MP = EC::MP, NPM1 = EC::NPM1;
+  constexpr int RB = EC::RB, TG = EC::TG, KO = EC::KO;
+  const StageArgs<R>& A = EA.s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int grp = tid / TG, q = tid - grp * TG;
+  char* gb = reinterpret_cast<char*>(smem_raw) + grp * EC::GB;
+  // wadg_phases / face_sum3 take the acoustic config's GroupSync (same TG and barrier id)
+  const GroupSync<AC> sync{1 + grp};
+  constexpr TabLayout L = tab_layout(N, M, RB);
+  const uint8_t* tab = A.tab;
+  const R* invfacN = reinterpret_cast<const R*>(tab + L.s_invfacN);
+  const R* facN = reinterpret_cast<const R*>(tab + L.s_facN);
+  const R* outN = reinterpret_cast<const R*>(tab + L.s_outN);
+  const R* invfacM = reinterpret_cast<const R*>(tab + L.s_invfacM);
+  const R* invfacNm1 = reinterpret_cast<const R*>(tab + L.s_invfacNm1);
+  const R* cfac = reinterpret_cast<const R*>(tab + L.s_cfac);
+  const uint16_t* fnode = reinterpret_cast<const uint16_t*>(tab + L.fnode);
+  const uint16_t* nbrvol = reinterpret_cast<const uint16_t*>(tab + L.nbrvol);
+  const uint16_t* padoff = reinterpret_cast<const uint16_t*>(tab + L.padoff);
+
+  const long long nelem = A.elem_end - A.elem_begin;
+  const int gw = grp % EC::GPW;
+  for (long long bw = (long long)blockIdx.x * EC::G + (grp - gw); bw < nelem; bw += (long long)gridDim.x * EC::G) {
+    const long long batch = bw + gw;
+    const long long k = A.elem_begin + batch;
+    const bool live = batch < nelem;  // sub-warp groups: idle groups run the phases on stale data, write nothing
+    long long pt_prev = 0;
+    (void)pt_prev;
+
+    // ---- A: loads.  Q block (9 NP), grad(lambda), neighbour ids and codes, material c'' = c / b!
+    if (live) {
+      if (A.mode != 2) {
+        const R* gq = A.Qin + k * 9 * NP;
+        for (int t = q; t < 9 * NP; t += TG) cp_async_real<R>(gb + (EC::EQ + t) * RB, gq + t);
+        for (int t = q; t < 12; t += TG) cp_async_real<R>(gb + (EC::O_GEO + t) * RB, A.geo + k * 12 + t);
+        if (q < 4) {
+          cp_async4(gb + 28 * RB + 4 * q, A.nbr + k * 4 + q);
+        }
+        if (q == 0) cp_async4(gb + 28 * RB + 16, A.code + k * 4);
+      }
+      for (int t = q; t < 3 * MP; t += TG) cp_async_real<R>(gb + (EC::ECM + t) * RB, EA.mat + k * 3 * MP + t);
+    }
+    cp_async_wait_all();
+    sync();
+    for (int t = q; t < 3 * MP; t += TG) {  // c'' = c / b!
+      char* p = gb + (EC::ECM + t) * RB;
+      st<R>(p, ld<R>(p) * __ldg(invfacM + t % MP));
+    }
+    if (A.mode != 2) {
+      for (int f = q; f < 4; f += TG) {  // outward normal, |grad lambda_f|
+        char* sg = gb + EC::O_GEO * RB;
+        const R gx = ld<R>(sg + (3 * f) * RB), gy = ld<R>(sg + (3 * f + 1) * RB), gz = ld<R>(sg + (3 * f + 2) * RB);
+        const R gl = sqrt(gx * gx + gy * gy + gz * gz), il = R(1) / gl;
+        st<R>(sg + (12 + 4 * f) * RB, -gx * il);
+        st<R>(sg + (13 + 4 * f) * RB, -gy * il);
+        st<R>(sg + (14 + 4 * f) * RB, -gz * il);
+        st<R>(sg + (15 + 4 * f) * RB, gl);
+      }
+      for (int z = q; z < 9; z += TG) st<R>(gb + (EC::EG + z * (NPM1 + 1)) * RB, R(0));  // zero slots of G''
+    }
+    sync();
+
+    R rr[9][KO];  // r''_x = r_x / a! of the lane's coefficients a = q + TG k
+    if (A.mode == 2) {
+      // WADG test hook: Qin = r[K][9][NP] (plain coefficients) -> rr
+#pragma unroll
+      for (int c = 0; c < 9; ++c)
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) {
+          const int a = q + TG * kk;
+          rr[c][kk] = (live && a < NP) ? A.Qin[k * 9 * NP + c * NP + a] * __ldg(invfacN + a) : R(0);
+        }
+    } else {
+      // ---- B1a: neighbour traces (9 fields) of every face node, issued before the volume phase
+      constexpr int NI1 = 4 * NFP, K1 = (NI1 + TG - 1) / TG;
+      R tn[K1][9];
+#pragma unroll
+      for (int kk = 0; kk < K1; ++kk) {
+        const int t = q + TG * kk;
+        const bool act = t < NI1;
+        const int tc = act ? t : 0;
+        const int f = tc / NFP, i = tc - f * NFP;
+        const int* nbs = reinterpret_cast<const int*>(gb + 28 * RB);
+        const int nb = nbs[f], code = reinterpret_cast<const uint8_t*>(nbs + 4)[f];
+#pragma unroll
+        for (int c = 0; c < 9; ++c) tn[kk][c] = R(0);
+        if (act && live && nb >= 0) {
+          const int vol = __ldg(nbrvol + code * NFP + i);
+          const R* qn = A.Qin + (long long)nb * 9 * NP + vol;
+#pragma unroll
+          for (int c = 0; c < 9; ++c) tn[kk][c] = __ldg(qn + c * NP);
+        }
+      }
+      // ---- B2: gradient combinations at degree N-1, g''_b = sum_j grad(l_j) . (...)_{b+e_j} / b!
+      {
+        R lg[12];
+#pragma unroll
+        for (int w = 0; w < 12; ++w) lg[w] = ld<R>(gb + (EC::O_GEO + w) * RB);
+        const ushort4* vg = reinterpret_cast<const ushort4*>(tab + L.vg);
+        const char* eq = gb + EC::EQ * RB;
+        for (int b = q; b < NPM1; b += TG) {
+          const ushort4 o = __ldg(vg + b);
+          const int off[4] = {o.x, o.y, o.z, o.w};
+          const R sc = __ldg(invfacNm1 + b);
+          R g[9];
+#pragma unroll
+          for (int c = 0; c < 9; ++c) g[c] = R(0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const R lx = lg[3 * j], ly = lg[3 * j + 1], lz = lg[3 * j + 2];
+            const char* p = eq + off[j];
+            const R v1 = ld<R>(p), v2 = ld<R>(p + NP * RB), v3 = ld<R>(p + 2 * NP * RB);
+            const R s11 = ld<R>(p + 3 * NP * RB), s22 = ld<R>(p + 4 * NP * RB), s33 = ld<R>(p + 5 * NP * RB);
+            const R s23 = ld<R>(p + 6 * NP * RB), s13 = ld<R>(p + 7 * NP * RB), s12 = ld<R>(p + 8 * NP * RB);
+            // r_v = div sigma (A_i^T d_i sigma), r_sigma = engineering strain (A_i d_i v)
+            g[0] = fma(lx, s11, fma(ly, s12, fma(lz, s13, g[0])));
+            g[1] = fma(lx, s12, fma(ly, s22, fma(lz, s23, g[1])));
+            g[2] = fma(lx, s13, fma(ly, s23, fma(lz, s33, g[2])));
+            g[3] = fma(lx, v1, g[3]);
+            g[4] = fma(ly, v2, g[4]);
+            g[5] = fma(lz, v3, g[5]);
+            g[6] = fma(lz, v2, fma(ly, v3, g[6]));
+            g[7] = fma(lz, v1, fma(lx, v3, g[7]));
+            g[8] = fma(ly, v1, fma(lx, v2, g[8]));
+          }
+#pragma unroll
+          for (int c = 0; c < 9; ++c) st<R>(gb + (EC::EG + c * (NPM1 + 1) + 1 + b) * RB, g[c] * sc);
+        }
+      }
+      sync();
+      // ---- C1: r''_c[a] = sum_j g''_c[a - e_j]  (elevation, zero slot for missing a - e_j)
+      {
+        const ushort4* ve = reinterpret_cast<const ushort4*>(tab + L.ve);
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) {
+          const int a = q + TG * kk;
+          if (a < NP) {
+            const ushort4 o = __ldg(ve + a);
+            const char* p0 = gb + o.x + EC::EG * RB;
+            const char* p1 = gb + o.y + EC::EG * RB;
+            const char* p2 = gb + o.z + EC::EG * RB;
+            const char* p3 = gb + o.w + EC::EG * RB;
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+              const int S = c * (NPM1 + 1) * RB;
+              rr[c][kk] = (ld<R>(p0 + S) + ld<R>(p1 + S)) + (ld<R>(p2 + S) + ld<R>(p3 + S));
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 9; ++c) rr[c][kk] = R(0);
+          }
+        }
+      }
+      sync();  // G'' dead: the flux arrays overlay it
+      // ---- B1b: fluxes of every face node -> F' = |grad l_f| c! F  in [batch b][face f][F_v[b], w[b]][NFP]
+      for (int z = q; z < 8; z += TG) st<R>(gb + (EC::EY + z * (NFP1 + 1)) * RB, R(0));  // zero slots of Y''
+#pragma unroll
+      for (int kk = 0; kk < K1; ++kk) {
+        const int t = q + TG * kk;
+        if (t < NI1) {
+          const int f = t / NFP, i = t - f * NFP;
+          const int own = __ldg(fnode + f * NFP + i);
+          const char* eq = gb + EC::EQ * RB + own;
+          const int nb = reinterpret_cast<const int*>(gb + 28 * RB)[f];
+          R qm[9], jq[9];
+#pragma unroll
+          for (int c = 0; c < 9; ++c) qm[c] = ld<R>(eq + c * NP * RB);
+          const bool bnd = nb < 0;  // traction-free mirror: v+ = v, sigma+ = -sigma (R26)
+#pragma unroll
+          for (int c = 0; c < 9; ++c) jq[c] = bnd ? (c < 3 ? R(0) : R(-2) * qm[c]) : tn[kk][c] - qm[c];
+          const char* gs = gb + (EC::O_GEO + 12 + 4 * f) * RB;
+          const R n1 = ld<R>(gs), n2 = ld<R>(gs + RB), n3 = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * __ldg(cfac + i);
+          // [[t]] = A_n^T [[sigma]]  (Voigt 3 s11, 4 s22, 5 s33, 6 s23, 7 s13, 8 s12)
+          const R t1 = n1 * jq[3] + n2 * jq[8] + n3 * jq[7];
+          const R t2 = n1 * jq[8] + n2 * jq[4] + n3 * jq[6];
+          const R t3 = n1 * jq[7] + n2 * jq[6] + n3 * jq[5];
+          // e = A_n [[v]], then A_n^T e
+          const R e1 = n1 * jq[0], e2 = n2 * jq[1], e3 = n3 * jq[2];
+          const R e4 = n3 * jq[1] + n2 * jq[2], e5 = n3 * jq[0] + n1 * jq[2], e6 = n2 * jq[0] + n1 * jq[1];
+          const R a1 = n1 * e1 + n2 * e6 + n3 * e5, a2 = n1 * e6 + n2 * e2 + n3 * e4, a3 = n1 * e5 + n2 * e4 + n3 * e3;
+          const R hv = R(0.5) * EA.tau_v, hs = R(0.5) * EA.tau_s;
+          const R fv[3] = {R(0.5) * t1 + hv * a1, R(0.5) * t2 + hv * a2, R(0.5) * t3 + hv * a3};
+          const R wv[3] = {R(0.5) * jq[0] + hs * t1, R(0.5) * jq[1] + hs * t2, R(0.5) * jq[2] + hs * t3};
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            st<R>(gb + (EC::EF + (b * 8 + 2 * f) * NFP + i) * RB, sc * fv[b]);
+            st<R>(gb + (EC::EF + (b * 8 + 2 * f + 1) * NFP + i) * RB, sc * wv[b]);
+          }
+        }
+      }
+      sync();
+      // ---- surface lift, three batches of 8 face arrays
+      R nrm[12];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) nrm[3 * f + d] = ld<R>(gb + (EC::O_GEO + 12 + 4 * f + d) * RB);
+      const R* cf2 = reinterpret_cast<const R*>(tab + L.s_cf2);
+      const ushort4* te = reinterpret_cast<const ushort4*>(tab + L.triele);
+      const uint2* lgt = reinterpret_cast<const uint2*>(tab + L.lg);
+      static_for<0, 3, 1>([&](auto bc) {
+        constexpr int b = decltype(bc)::value;
+        constexpr int FB = EC::EF + b * 8 * NFP;  // this batch's 8 flux arrays (stride NFP)
+        // C2: Y''[ff][d] = (sum_s F'[ff][d + e_s]) / (d!)^2
+        face_sum3<EC, R, NFP1, FB, NFP, EC::EY + 1, NFP1 + 1, true>(
+            gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(N - 1),
+            reinterpret_cast<const R*>(tab + L.s_invf2));
+        sync();
+        // C3: layer 0, w'_0[c] = (2N+3) F'[c] + (c!)^2 sum_s Y''[c - e_s]
+        for (int c = q; c < NFP; c += TG) {
+          const ushort4 o = __ldg(te + c);
+          const R sc = __ldg(cf2 + c);
+#pragma unroll
+          for (int ff = 0; ff < 8; ++ff) {
+            const char* ya = gb + (EC::EY + ff * (NFP1 + 1)) * RB;
+            const R y = ld<R>(ya + o.x) + ld<R>(ya + o.y) + ld<R>(ya + o.z);
+            const R F = ld<R>(gb + (FB + ff * NFP + c) * RB);
+            st<R>(gb + (EC::EL + ff * NP + c) * RB, fma(sc, y, R(2 * N + 3) * F));
+          }
+        }
+        sync();
+        // D: lift layers j = 1..N (pre-multiplied by lam_j: s_j = -j/(j+1) R(s_{j-1}))
+        static_for<1, N + 1, 1>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          constexpr int m = N - j;
+          face_sum3<EC, R, cnp2(m), EC::EL + layer_off(N, j - 1), NP, EC::EL + layer_off(N, j), NP, false, -j, j + 1>(
+              gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(m), static_cast<const R*>(nullptr));
+          sync();
+        });
+        // E: gather the 4 faces' lifts: r''_v[b] += S_v/(a!)^2, r''_sigma += A_n(f)[:, b] S_w/(a!)^2
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) {
+          const int a = q + TG * kk;
+          if (a < NP) {
+            const uint2 e = __ldg(lgt + a);
+            const int lo[4] = {(int)(e.x & 0xFFFF), (int)(e.x >> 16), (int)(e.y & 0xFFFF), (int)(e.y >> 16)};
+            const R i1 = __ldg(invfacN + a), i2 = i1 * i1;
+            R sv = R(0), sx = R(0), sy = R(0), sz = R(0);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+              const R wp = ld<R>(gb + (EC::EL + (2 * f) * NP) * RB + lo[f]);
+              const R wu = ld<R>(gb + (EC::EL + (2 * f + 1) * NP) * RB + lo[f]);
+              sv += wp;
+              sx = fma(nrm[3 * f], wu, sx);
+              sy = fma(nrm[3 * f + 1], wu, sy);
+              sz = fma(nrm[3 * f + 2], wu, sz);
+            }
+            rr[b][kk] = fma(sv, i2, rr[b][kk]);
+            // column b of A_n: b = 0: s11 n1, s13 n3, s12 n2; b = 1: s22 n2, s23 n3, s12 n1; b = 2: s33 n3, s23 n2, s13 n1
+            if constexpr (b == 0) {
+              rr[3][kk] = fma(sx, i2, rr[3][kk]);
+              rr[7][kk] = fma(sz, i2, rr[7][kk]);
+              rr[8][kk] = fma(sy, i2, rr[8][kk]);
+            } else if constexpr (b == 1) {
+              rr[4][kk] = fma(sy, i2, rr[4][kk]);
+              rr[6][kk] = fma(sz, i2, rr[6][kk]);
+              rr[8][kk] = fma(sx, i2, rr[8][kk]);
+            } else {
+              rr[5][kk] = fma(sz, i2, rr[5][kk]);
+              rr[6][kk] = fma(sy, i2, rr[6][kk]);
+              rr[7][kk] = fma(sx, i2, rr[7][kk]);
+            }
+          }
+        }
+        sync();
+      });
+    }
+
+    // ---- WADG: ten scalar applications P_N(w r''), results combined per field, LSRK per field.  One runtime
+    //      loop (the application is inlined once); register arrays are indexed through select chains.
+    auto pick = [&](const R (&arr)[9][KO], int c, int kk) {
+      R v = arr[0][kk];
+#pragma unroll
+      for (int z = 1; z < 9; ++z)
+        if (c == z) v = arr[z][kk];
+      return v;
+    };
+    R wl[KO];  // W_lambda(s), s = r_s11 + r_s22 + r_s33
+#pragma unroll 1
+    for (int app = 0; app < 10; ++app) {
+      // app 0..2: rho^-1 on v_app; app 3: lambda on s; app 4..9: mu on sigma_{app-4} (field app-1)
+      const int w = app < 3 ? 0 : app == 3 ? 1 : 2;
+      const int fld = app < 3 ? app : app - 1;
+      R x[KO], y[KO];
+#pragma unroll
+      for (int kk = 0; kk < KO; ++kk) x[kk] = app == 3 ? (rr[3][kk] + rr[4][kk]) + rr[5][kk] : pick(rr, fld, kk);
+      if constexpr (M == 0) {
+        // constant weight (BBDG): P_N(w r) = w_0 r, r = a! r''
+        const R w0 = ld<R>(gb + (EC::ECM + w * MP) * RB);
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) y[kk] = w0 * __ldg(facN + cmin(q + TG * kk, NP - 1)) * x[kk];
+      } else {
+        zero_region<AC>(gb, q, AC::Y_RPP, AC::NS);
+        sync();
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) {
+          const int a = q + TG * kk;
+          if (a < NP) st<R>(gb + AC::Y_RPP * RB + __ldg(padoff + a), x[kk]);
+        }
+        for (int b = q; b < MP; b += TG) st<R>(gb + (AC::O_C + b) * RB, ld<R>(gb + (EC::ECM + w * MP + b) * RB));
+        sync();
+        R ob[KO];
+        wadg_phases<AC, R>(gb, q, A, sync, pt_prev, ob);
+        constexpr int RES = AC::TRIPLE ? AC::tlev(N) : wadg_result<AC>();
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) {
+          const int a = cmin(q + TG * kk, NP - 1);
+          const int cs = AC::TRIPLE ? (int)__ldg(reinterpret_cast<const uint32_t*>(tab + L.sho) + a) : a;
+          const R sc = AC::TRIPLE ? __ldg(outN + a) : ob[kk];
+          y[kk] = ld<R>(gb + (RES + cs) * RB) * sc;
+        }
+        sync();
+      }
+      if (app == 3) {
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) wl[kk] = y[kk];
+        continue;
+      }
+      // ds_i = W_lambda(s) + 2 W_mu(r_si) (normal stresses, i < 3), W_mu(r_si) (shear)
+      if (app >= 4 && app <= 6) {
+#pragma unroll
+        for (int kk = 0; kk < KO; ++kk) y[kk] = fma(R(2), y[kk], wl[kk]);
+      }
+#pragma unroll
+      for (int kk = 0; kk < KO; ++kk) {
+        const int a = q + TG * kk;
+        if (live && a < NP) {
+          const long long gi = k * 9 * NP + fld * NP + a;
+          if (A.mode == 0) {
+            // LSRK state read here (residual: first touch; Q_in: L2), not held in registers across the
+            // ten applications (measured: 255 registers and spills with it resident)
+            const R r = fma(A.rk_a, __ldcs(A.res + gi), A.dt * y[kk]);
+            A.res[gi] = r;
+            A.Qout[gi] = fma(A.rk_b, r, __ldg(A.Qin + gi));
+          } else {
+            A.Qout[gi] = y[kk];
+          }
+        }
+      }
+    }
+    sync();
+  }
+}
+
+}  // namespace bbw

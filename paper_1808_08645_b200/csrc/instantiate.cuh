@@ -3,6 +3,7 @@
 #include <type_traits>
 
 #include "dispatch.hpp"
+#include "elastic_kernel.cuh"
 #include "stage_kernel.cuh"
 
 namespace bbw {
@@ -34,8 +35,29 @@ struct Inst {
       return 1;
     return nb > 0 ? nb : 1;
   }
+  using EC = ElasticCfg<N, M, R>;
+  static cudaError_t prepare_e() {
+    return cudaFuncSetAttribute(elastic_stage_kernel<EC, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, EC::SMEM_BYTES);
+  }
+  static cudaError_t launch_e(const void* args, int grid, cudaStream_t s) {
+    const ElasticArgs<R>& a = *static_cast<const ElasticArgs<R>*>(args);
+    elastic_stage_kernel<EC, R><<<grid, EC::T, EC::SMEM_BYTES, s>>>(a);
+    return cudaGetLastError();
+  }
+  static int blocks_e() {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, elastic_stage_kernel<EC, R>, EC::T, EC::SMEM_BYTES) != cudaSuccess)
+      return 1;
+    return nb > 0 ? nb : 1;
+  }
   static KernelSet get() {
     KernelSet k;
+    k.launch_elastic = &launch_e;
+    k.prepare_elastic = &prepare_e;
+    k.elastic_blocks_per_sm = &blocks_e;
+    k.elastic_smem_bytes = EC::SMEM_BYTES;
+    k.elastic_elems_per_cta = EC::G;
+    k.elastic_threads = EC::T;
     k.launch_stage = &launch;
     k.launch_pack = &pack;
     k.prepare = &prepare;

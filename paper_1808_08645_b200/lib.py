@@ -62,6 +62,7 @@ def _load() -> ctypes.CDLL:
         "bbwadg_default_options": (None, [P(bbwadg_options)]),
         "bbwadg_setup": (S, [P(bbwadg_mesh), I, I, V, P(bbwadg_options), P(ctx_p)]),
         "bbwadg_setup_group": (S, [P(bbwadg_mesh), I, I, V, P(bbwadg_options), I, V]),
+        "bbwadg_elastic_setup": (S, [P(bbwadg_mesh), I, I, V, V, V, P(bbwadg_options), P(ctx_p)]),
         "bbwadg_set_state": (S, [ctx_p, V, I]),
         "bbwadg_get_state": (S, [ctx_p, V, I]),
         "bbwadg_set_source": (S, [ctx_p, V]),
@@ -124,6 +125,14 @@ def bbwadg_setup(vertices, elements, N: int, M: int, c2, opts: bbwadg_options):
     m = bbwadg_mesh(vertices.shape[0], _ptr(vertices), elements.shape[0], _ptr(elements))
     ctx = ctypes.c_void_p()
     _check(_L.bbwadg_setup(ctypes.byref(m), N, M, _ptr(c2), ctypes.byref(opts), ctypes.byref(ctx)))
+    return ctx
+
+
+def bbwadg_elastic_setup(vertices, elements, N: int, M: int, rho_inv, lam, mu, opts: bbwadg_options):
+    m = bbwadg_mesh(vertices.shape[0], _ptr(vertices), elements.shape[0], _ptr(elements))
+    ctx = ctypes.c_void_p()
+    _check(_L.bbwadg_elastic_setup(ctypes.byref(m), N, M, _ptr(rho_inv), _ptr(lam), _ptr(mu), ctypes.byref(opts),
+                                   ctypes.byref(ctx)))
     return ctx
 
 

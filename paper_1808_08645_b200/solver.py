@@ -6,6 +6,9 @@
     s.run(t0=0.0, dt=dt, nsteps=100)
     Q = s.get_state()                                      # numpy, global element order
 
+    e = ElasticSolver(vertices, elements, N=5, M=1, rho_inv=ri, lam=la, mu=mu)  # [K, Np(M)] each
+    e.set_state(Q9)                                        # [K,9,Np]: v1..3, s11 s22 s33 s23 s13 s12
+
 No arithmetic of the method happens here: every call forwards to libbbwadg.so.
 """
 from __future__ import annotations
@@ -18,6 +21,8 @@ from . import lib as L
 
 
 class Solver:
+    NF = 4  # fields per element: p, u_x, u_y, u_z
+
     def __init__(self, vertices, elements, N: int, M: int, c2, *, dtype: str = "f64", tau_p: float = 1.0,
                  tau_u: float = 1.0, device: int = 0, stream=None, rank: int = 0, world_size: int = 1,
                  nccl_id: bytes | None = None, partition=None, check_c2: bool = True, c2_gids=None):
@@ -71,21 +76,21 @@ class Solver:
         return np.float64 if self.dtype == "f64" else np.float32
 
     def set_state(self, Q):
-        """Q: numpy [K_global,4,Np] (global order) or a CUDA tensor [K_local,4,Np] (local order)."""
+        """Q: numpy [K_global,NF,Np] (global order) or a CUDA tensor [K_local,NF,Np] (local order)."""
         if isinstance(Q, np.ndarray):
             if Q.shape[0] != self.K_local:
                 Q = Q[self.global_ids]
             Q = np.ascontiguousarray(Q, dtype=self._host_dtype())
             L.bbwadg_set_state(self.ctx, Q, 0)
         else:
-            L.bbwadg_set_state(self.ctx, self._check_dev(Q, (self.K_local, 4, self.Np), "Q"), 1)
+            L.bbwadg_set_state(self.ctx, self._check_dev(Q, (self.K_local, self.NF, self.Np), "Q"), 1)
 
     def get_state(self, device: bool = False):
         if device:
-            out = self.torch.empty((self.K_local, 4, self.Np), dtype=self.tdtype, device=self.device)
+            out = self.torch.empty((self.K_local, self.NF, self.Np), dtype=self.tdtype, device=self.device)
             L.bbwadg_get_state(self.ctx, out, 1)
             return out
-        out = np.empty((self.K_local, 4, self.Np), dtype=self._host_dtype())
+        out = np.empty((self.K_local, self.NF, self.Np), dtype=self._host_dtype())
         L.bbwadg_get_state(self.ctx, out, 0)
         return out
 
@@ -106,13 +111,14 @@ class Solver:
 
     # -------------------------------------------------------------------------------- compute
     def rhs(self, Q_dev, t: float = 0.0):
-        Q_dev = self._check_dev(Q_dev, (self.K_local, 4, self.Np), "Q")
+        Q_dev = self._check_dev(Q_dev, (self.K_local, self.NF, self.Np), "Q")
         out = self.torch.empty(Q_dev.shape, dtype=self.tdtype, device=self.device)
         L.bbwadg_rhs(self.ctx, Q_dev, t, out)
         return out
 
     def wadg_apply(self, r_dev):
-        r_dev = self._check_dev(r_dev, (self.K_local, self.Np), "r")
+        shape = (self.K_local, self.Np) if self.NF == 4 else (self.K_local, self.NF, self.Np)
+        r_dev = self._check_dev(r_dev, shape, "r")
         out = self.torch.empty(r_dev.shape, dtype=self.tdtype, device=self.device)
         L.bbwadg_wadg_apply(self.ctx, r_dev, out)
         return out
@@ -142,3 +148,42 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+class ElasticSolver(Solver):
+    """Elastic BBWADG (Eq. ewave / ewadg) through bbwadg_elastic_setup: state
+    [K, 9, Np] = (v_1, v_2, v_3, s11, s22, s33, s23, s13, s12); material rho_inv, lam, mu [K, Np(M)];
+    tau_s / tau_v the stress / velocity penalties.  Single GPU."""
+
+    NF = 9
+
+    def __init__(self, vertices, elements, N: int, M: int, rho_inv, lam, mu, *, dtype: str = "f64",
+                 tau_v: float = 1.0, tau_s: float = 1.0, device: int = 0, stream=None, check: bool = True):
+        import torch
+
+        self.torch = torch
+        self.N, self.M = int(N), int(M)
+        self.Np, self.Mp = comb(N + 3, 3), comb(M + 3, 3)
+        self.dtype = dtype
+        self.tdtype = torch.float64 if dtype == "f64" else torch.float32
+        self.device = torch.device("cuda", device)
+        self._v = np.ascontiguousarray(vertices, dtype=np.float64)
+        self._e = np.ascontiguousarray(elements, dtype=np.int64)
+        mats = []
+        for name, a in (("rho_inv", rho_inv), ("lam", lam), ("mu", mu)):
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            if a.shape != (self._e.shape[0], self.Mp):
+                raise ValueError(f"{name} must have shape [K, {self.Mp}]")
+            mats.append(a)
+        o = L.bbwadg_default_options()
+        o.dtype = L.BBWADG_F64 if dtype == "f64" else L.BBWADG_F32
+        o.tau_p, o.tau_u, o.device = float(tau_s), float(tau_v), int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        self.stream = stream
+        o.check_c2 = 1 if check else 0
+        self.ctx = L.bbwadg_elastic_setup(self._v, self._e, self.N, self.M, *mats, o)
+        info = self.info()
+        self.K_local = info["num_elements_local"]
+        self.global_ids = info["global_ids"]
