@@ -338,6 +338,8 @@ def run_ours(args):
         out["cpu_baseline"] = cpu_baseline(N, M, args.cpu_seconds, extras=True)
     if rank == 0 and not args.no_config4:
         out["config4"] = config4_runs(args, dev)
+    if rank == 0 and args.elastic:
+        out["elastic"] = elastic_runs(args, dev)
     if rank == 0 and not args.no_sweep:
         out["sweep"] = sweep(args, dev)
     if rank == 0:
@@ -389,6 +391,66 @@ def config4_runs(args, dev):
         s.close()
     out["workload"] = (f"config4: Kuhn n={n} ({len(e):,} tets), N={N}, M={M}, layered c^2 1/1.5/2.25 (sub-cell "
                        f"jumps), Gaussian pulse")
+    return out
+
+
+def elastic_runs(args, dev):
+    """Elastic BBWADG: n=56 Kuhn mesh (1,053,696 tets), smooth Lame fields
+    (workloads.elastic.smooth_material) projected to P^M, Gaussian pressure pulse in the normal stresses;
+    the paper's elastic runtime study uses M = 1, 2.  3 warm-up + 10 timed steps per line,
+    clocks sampled during the timed steps; value = 9 K Np 5 steps / device time."""
+    import torch
+
+    from paper_1808_08645_b200 import ElasticSolver
+    from workloads import elastic as ew
+    from workloads import kuhn
+
+    n = args.elastic_n
+    v, e = kuhn.kuhn_mesh(n)
+    peaks, _ = load_peaks()
+    out = {"workload": f"elastic: Kuhn n={n} ({len(e):,} tets), smooth rho^-1/lambda/mu, pressure pulse in s11/s22/s33"}
+    for spec in args.elastic.split(","):
+        N, M, dt_name = spec.split(":")
+        N, M = int(N), int(M)
+        Np = comb(N + 3, 3)
+        mats = ew.smooth_material(v, e, M, device=dev)
+        from workloads._l2fit import l2_fit
+
+        g = torch.from_numpy(l2_fit(v, e, lambda x, y, z, xp=np: xp.exp(-50.0 * (x * x + y * y + z * z)), N,
+                                    device=dev)).to(dev)
+        Q0 = torch.zeros((len(e), 9, Np), dtype=torch.float64, device=dev)
+        Q0[:, 3:6] = -g[:, None, :]  # the pulse of workloads.elastic.gaussian_pulse, built on the device
+        del g
+        s = ElasticSolver(v, e, N, M, *mats, dtype=dt_name, device=dev.index, stream=torch.cuda.current_stream(dev))
+        s.set_state(Q0 if dt_name == "f64" else Q0.float())
+        del Q0
+        h_min = 2.0 / n / (1 + np.sqrt(2) + np.sqrt(3))
+        cp = np.sqrt((mats[1].max() + 2 * mats[2].max()) * mats[0].max())
+        dt = 0.5 * h_min / (cp * (N + 1) ** 2)
+        for i in range(3):
+            s.step(i * dt, dt)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev.index) as clk:
+            torch.cuda.synchronize()
+            a.record()
+            for i in range(10):
+                s.step((3 + i) * dt, dt)
+            b.record()
+            torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        info = s.info()
+        gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
+        out[f"N{N}M{M}{dt_name}"] = {
+            "value": 9.0 * len(e) * Np * 5 / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(gbs / peaks["hbm_gbs"], 4), "kernel": f"bbw::elastic_stage_kernel<N={N},M={M},{dt_name}>",
+                         "algorithmic_bytes_per_launch": info["algorithmic_bytes_per_stage"],
+                         "achieved_tflops": round(info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12, 3)},
+            "warmup": 3, "steps": 10, "gpu_launches": 50, "clocks": clk.summary()}
+        s.close()
+        del s
+        torch.cuda.empty_cache()
     return out
 
 
@@ -579,6 +641,9 @@ def main():
     ap.add_argument("--sweep-warmup", type=int, default=3)
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--no-config4", action="store_true", help="skip the config-4 fp64/fp32 extra lines")
+    ap.add_argument("--elastic", default="7:2:f64,7:2:f32,5:1:f64,3:1:f64,9:2:f64",
+                    help="elastic BBWADG lines N:M:dtype (comma separated; '' skips them)")
+    ap.add_argument("--elastic-n", type=int, default=56)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus != world and not (args.gpus == 1 and world == 1):

@@ -38,19 +38,26 @@ struct ElasticCfg {
   // application at AC::O_C, WADG work region from AC::O_X), with the elastic volume/surface arrays
   // overlaying [O_X, ...) and the three material arrays after everything
   static constexpr int O_GEO = 0, O_X = AC::O_X;
-  static constexpr int EQ = O_X;                     // Q_in, 9 NP (volume / surface phases)
+  static constexpr int EQ = O_X;                     // Q_in, 9 NP (volume phase and the flux phase)
   static constexpr int EG = EQ + 9 * NP;             // 9 gradient arrays, each (zero slot + NPM1)
-  static constexpr int EF = EQ + 9 * NP;             // fluxes [3 batches][4 faces][2][NFP] (G dead)
-  static constexpr int EY = EF + 24 * NFP;           // Y'' [8][NFP1 + 1]
-  static constexpr int EL = rup(EY + 8 * (NFP1 + 1), VEC);  // lift layers [8][NP]
-  static constexpr int EVS_END = cmax(EG + 9 * (NPM1 + 1), EL + 8 * NP);
+  // surface phase: all 24 flux arrays are formed while Q_in is live, then Y'' and the lift layers
+  // overlay the dead Q_in block
+  static constexpr int EY = O_X;                             // Y'' [8][NFP1 + 1]
+  static constexpr int EL = rup(EY + 8 * (NFP1 + 1), VEC);   // lift layers [8][NP]
+  static constexpr int EF = rup(cmax(EQ + 9 * NP, EL + 8 * NP), VEC);  // fluxes [3 batches][4 faces][2][NFP]
+  static constexpr int EVS_END = cmax(EG + 9 * (NPM1 + 1), EF + 24 * NFP);
   static constexpr int ECM = rup(cmax(EVS_END, AC::PER_E), VEC);  // rho^-1'', lambda'', mu'' [3][MP]
   static constexpr int PER_E = rup(ECM + 3 * MP, VEC);
   static constexpr int EB = PER_E * RB;
   static constexpr int GB = EB;
   static constexpr int SMEM_BYTES = G * GB + 8 * G;
-  // resident CTAs per SM allowed by shared memory (227 KB per SM usable): caps registers per thread
-  static constexpr int MINB = cmax(1, cmin(8, (227 * 1024) / SMEM_BYTES));
+  // resident CTAs per SM allowed by shared memory (228 KB per SM, 1 KB reserved per CTA): the launch
+  // bounds cap registers so that registers do not limit occupancy below that (BBW_EMINB overrides)
+#ifdef BBW_EMINB
+  static constexpr int MINB = BBW_EMINB;
+#else
+  static constexpr int MINB = cmax(1, cmin(8, (228 * 1024) / (SMEM_BYTES + 1024)));
+#endif
   static_assert(SMEM_BYTES <= 227 * 1024, "elastic element block exceeds shared memory");
 };
 
@@ -220,7 +227,6 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
       }
       sync();  // G'' dead: the flux arrays overlay it
       // ---- B1b: fluxes of every face node -> F' = |grad l_f| c! F  in [batch b][face f][F_v[b], w[b]][NFP]
-      for (int z = q; z < 8; z += TG) st<R>(gb + (EC::EY + z * (NFP1 + 1)) * RB, R(0));  // zero slots of Y''
 #pragma unroll
       for (int kk = 0; kk < K1; ++kk) {
         const int t = q + TG * kk;
@@ -255,7 +261,8 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
           }
         }
       }
-      sync();
+      sync();  // Q_in dead: Y'' and the lift layers overlay it
+      for (int z = q; z < 8; z += TG) st<R>(gb + (EC::EY + z * (NFP1 + 1)) * RB, R(0));  // zero slots of Y''
       // ---- surface lift, three batches of 8 face arrays
       R nrm[12];
 #pragma unroll
@@ -348,9 +355,19 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
       // app 0..2: rho^-1 on v_app; app 3: lambda on s; app 4..9: mu on sigma_{app-4} (field app-1)
       const int w = app < 3 ? 0 : app == 3 ? 1 : 2;
       const int fld = app < 3 ? app : app - 1;
-      R x[KO], y[KO];
+      R x[KO], y[KO], pres[KO], pq[KO];
 #pragma unroll
       for (int kk = 0; kk < KO; ++kk) x[kk] = app == 3 ? (rr[3][kk] + rr[4][kk]) + rr[5][kk] : pick(rr, fld, kk);
+      // LSRK state of this application's output field, requested now and consumed after the application
+      // (its HBM / L2 latency overlaps the product and the sweeps; not held across the ten applications)
+#pragma unroll
+      for (int kk = 0; kk < KO; ++kk) {
+        const int a = q + TG * kk;
+        const bool ok = A.mode == 0 && app != 3 && live && a < NP;
+        const long long gi = k * 9 * NP + fld * NP + a;
+        pres[kk] = ok ? __ldcs(A.res + gi) : R(0);
+        pq[kk] = ok ? __ldg(A.Qin + gi) : R(0);
+      }
       if constexpr (M == 0) {
         // constant weight (BBDG): P_N(w r) = w_0 r, r = a! r''
         const R w0 = ld<R>(gb + (EC::ECM + w * MP) * RB);
@@ -394,11 +411,9 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
         if (live && a < NP) {
           const long long gi = k * 9 * NP + fld * NP + a;
           if (A.mode == 0) {
-            // LSRK state read here (residual: first touch; Q_in: L2), not held in registers across the
-            // ten applications (measured: 255 registers and spills with it resident)
-            const R r = fma(A.rk_a, __ldcs(A.res + gi), A.dt * y[kk]);
+            const R r = fma(A.rk_a, pres[kk], A.dt * y[kk]);
             A.res[gi] = r;
-            A.Qout[gi] = fma(A.rk_b, r, __ldg(A.Qin + gi));
+            A.Qout[gi] = fma(A.rk_b, r, pq[kk]);
           } else {
             A.Qout[gi] = y[kk];
           }
