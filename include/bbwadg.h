@@ -92,7 +92,11 @@ typedef struct {
   int partition[3];      /* cut counts per axis for the recursive coordinate bisection
                             (product must equal world_size); {0,0,0} = automatic */
   int check_c2;          /* 1 (default): reject non-positive c^2_M at setup */
-  int reserved0;
+  int halo_transport;    /* partition faces (world_size > 1 or groups): 0 (default) = pack (p, u.n) per
+                            face + NCCL send/recv (device copies in groups); 1 = PEER READS: the stage
+                            kernel reads the owner partition's Q_in in place (same device: groups; other
+                            processes / GPUs: CUDA IPC, bbwadg_ipc_get_handles / bbwadg_ipc_open_peer), no
+                            pack, no collective, bitwise equal to the single-partition run */
   const int64_t* c2_gids; /* optional (multi-GPU memory): when non-NULL, c2_coeffs of bbwadg_setup holds
                              c2_rows rows, row i for global element c2_gids[i] (e.g. this rank's elements
                              from bbwadg_partition_plan); every element the rank owns must be present
@@ -190,6 +194,21 @@ bbwadg_status bbwadg_elastic_setup(const bbwadg_mesh* mesh, int N, int M, const 
 bbwadg_status bbwadg_setup_group(const bbwadg_mesh* mesh, int N, int M, const double* c2_coeffs,
                                  const bbwadg_options* opts, int nparts, bbwadg_ctx* out /* [nparts] */);
 bbwadg_status bbwadg_group_step(bbwadg_ctx* ctxs, int nparts, double t, double dt);
+
+/* ---- peer-read halo across processes (halo_transport = 1, world_size > 1): CUDA IPC mapping of the
+ * partitions' state buffers, so the stage kernel reads neighbour face traces from the owner's Q_in in
+ * place (over NVLink between GPUs; also valid for several processes sharing one GPU).
+ * bbwadg_ipc_get_handles: out[2][64] = cudaIpcMemHandle_t of this context's two state buffers.
+ * bbwadg_ipc_open_peer:   map the handles of rank `peer` (from its bbwadg_ipc_get_handles, exchanged by
+ *                         the caller); every rank that owns a neighbour of this partition must be opened.
+ * bbwadg_stage:           one LSRK45 stage s (0..4) of the state at stage time t + c_s dt.  Between two
+ *                         stages every rank must have finished the previous one before any rank starts the
+ *                         next (the caller's barrier + bbwadg_synchronize), because the kernel reads the
+ *                         peers' stage inputs; bbwadg_step refuses IPC peer contexts for that reason.
+ *                         Works for every context (s = 0..4 in order is one bbwadg_step). */
+bbwadg_status bbwadg_ipc_get_handles(bbwadg_ctx ctx, void* out);
+bbwadg_status bbwadg_ipc_open_peer(bbwadg_ctx ctx, int peer, const void* handles);
+bbwadg_status bbwadg_stage(bbwadg_ctx ctx, int s, double t, double dt);
 
 /* ---- host-only helpers (no GPU needed) */
 /* Partition plan of rank `rank` among nparts (the same recursive coordinate bisection and

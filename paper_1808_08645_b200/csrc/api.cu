@@ -80,6 +80,12 @@ struct bbwadg_ctx_s {
   int* d_sendfaces = nullptr;
   int* d_flag = nullptr;
   unsigned long long* d_ptime = nullptr;  // phase timing counters (BBW_PHASE_TIMING builds)
+  // peer-read halo (halo_transport 1): owner-rank / owner-local id per ghost slot, and the peers' two
+  // state buffers (same-process group members, or CUDA-IPC mappings of other processes)
+  int transport = 0;
+  int* d_gmap = nullptr;
+  void* peer_q[8][2] = {};
+  bool peer_ipc[8] = {};
   // multi-GPU
   nccl::Comm comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -124,6 +130,10 @@ void fill_args(bbwadg_ctx c, StageArgs<R>& a) {
   a.ghost = static_cast<const R*>(c->d_ghost);
   a.src = static_cast<const R*>(c->d_src);
   a.tab = static_cast<const uint8_t*>(c->d_tab);
+  if (c->transport == 1 && c->d_gmap) {
+    a.gmap = c->d_gmap;
+    for (int r = 0; r < 8; ++r) a.peer[r] = static_cast<const R*>(c->peer_q[r][c->cur]);
+  }
   const HostTables& T = c->tables;
   a.tau_p = (R)c->tau_p;
   a.tau_u = (R)c->tau_u;
@@ -254,6 +264,15 @@ bbwadg_status full_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, dou
   static const char* kNames[3] = {"bbwadg stage (LSRK)", "bbwadg rhs", "bbwadg wadg_apply"};
   NvtxRange range(kNames[mode < 0 || mode > 2 ? 0 : mode]);
   const Part& P = c->part;
+  if (P.nparts > 1 && c->transport == 1) {
+    // peer reads: the boundary elements read the owners' Q_in in place (the caller guarantees the peers
+    // finished writing it: same stream for groups, a barrier between stages across processes)
+    for (int r = 0; r < P.nparts; ++r)
+      if (r != P.rank && P.recv_off[r + 1] > P.recv_off[r] && !c->peer_q[r][c->cur])
+        return fail(c, BBWADG_ERR_INVALID_ARG, "peer-read halo: a neighbour partition's state is not mapped");
+    if (Qin != c->d_Q[c->cur]) return fail(c, BBWADG_ERR_INVALID_ARG, "peer-read halo works on the context state only");
+    return launch_pass(c, mode, Qin, Qout, 0, P.K_local, rk_a, rk_b, dt, tstage);
+  }
   if (P.nparts > 1 && c->comm) {
     bbwadg_status s = halo_nccl(c, Qin);
     if (s) return s;
@@ -473,6 +492,11 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
     CUDA_TRY(c.get(), cudaMemset(c->d_ptime, 0, 32 * sizeof(unsigned long long)));
   }
   const int64_t nghost = P.num_ghost(), nsend = P.send_off.empty() ? 0 : P.send_off.back();
+  c->transport = o.halo_transport;
+  if (c->transport == 1 && nghost > 0) {
+    CUDA_TRY(c.get(), cudaMalloc(&c->d_gmap, sizeof(int) * 2 * nghost));
+    CUDA_TRY(c.get(), cudaMemcpy(c->d_gmap, P.gmap.data(), sizeof(int) * 2 * nghost, cudaMemcpyHostToDevice));
+  }
   const size_t per_face = 2 * (size_t)c->Nfp * c->rb;  // halo: p and u.n per face node
   if (nghost > 0) CUDA_TRY(c.get(), cudaMalloc(&c->d_ghost, nghost * per_face));
   if (nsend > 0) {
@@ -494,6 +518,10 @@ bbwadg_status prepare_global(const bbwadg_mesh* mesh, int N, int M, const double
   if (opts && opts->dtype != BBWADG_F64 && opts->dtype != BBWADG_F32)
     return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "dtype must be BBWADG_F64 or BBWADG_F32");
   if (opts && (opts->tau_p < 0 || opts->tau_u < 0)) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "tau must be >= 0");
+  if (opts && (opts->halo_transport < 0 || opts->halo_transport > 1))
+    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "halo_transport must be 0 (pack + NCCL) or 1 (peer reads)");
+  if (opts && opts->halo_transport == 1 && nparts > 8)
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "peer-read halo supports up to 8 partitions (one NVLink domain)");
   g.K = mesh->num_elements;
   g.nv = mesh->num_vertices;
   g.V = mesh->vertices;
@@ -530,8 +558,8 @@ bbwadg_status bbwadg_setup(const bbwadg_mesh* mesh, int N, int M, const double* 
   if (opts) o = *opts;
   if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size)
     return fail(nullptr, BBWADG_ERR_INVALID_ARG, "rank/world_size invalid");
-  if (o.world_size > 1 && !o.nccl_unique_id)
-    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "world_size > 1 needs nccl_unique_id");
+  if (o.world_size > 1 && o.halo_transport == 0 && !o.nccl_unique_id)
+    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "world_size > 1 needs nccl_unique_id (halo_transport 0)");
   // argument and mesh validation first (host only), then the device
   GlobalMesh g;
   bbwadg_status s = prepare_global(mesh, N, M, c2_coeffs, &o, o.world_size, g);
@@ -541,7 +569,7 @@ bbwadg_status bbwadg_setup(const bbwadg_mesh* mesh, int N, int M, const double* 
   s = setup_one(g, N, M, c2_coeffs, o, o.rank, o.world_size, nullptr, out);
   if (s) return s;
   bbwadg_ctx c = *out;
-  if (o.world_size > 1) {
+  if (o.world_size > 1 && o.halo_transport == 0) {
     std::string why;
     if (!nccl::load(why)) {
       bbwadg_destroy(c);
@@ -678,9 +706,59 @@ bbwadg_status bbwadg_wadg_apply(bbwadg_ctx c, const void* r_dev, void* out_dev) 
   return launch_pass(c, 2, r_dev, out_dev, 0, c->part.K_local, 0, 0, 0, 0);
 }
 
+bbwadg_status bbwadg_stage(bbwadg_ctx c, int s, double t, double dt) {
+  if (!c || s < 0 || s > 4) return fail(c, BBWADG_ERR_INVALID_ARG, "bad arguments");
+  if (c->group) return fail(c, BBWADG_ERR_INVALID_ARG, "use bbwadg_group_step for group contexts");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  bbwadg_status st = full_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], RK_A[s], RK_B[s], dt, t + RK_C[s] * dt);
+  if (st) return st;
+  c->cur ^= 1;
+  if (s == 4) {
+    c->steps++;
+    c->t = t + dt;
+  }
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_ipc_get_handles(bbwadg_ctx c, void* out) {
+  if (!c || !out) return fail(c, BBWADG_ERR_INVALID_ARG, "null argument");
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  for (int b = 0; b < 2; ++b) {
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->d_Q[b]));
+    std::memcpy(static_cast<char*>(out) + 64 * b, &h, 64);
+  }
+  return BBWADG_OK;
+}
+
+bbwadg_status bbwadg_ipc_open_peer(bbwadg_ctx c, int peer, const void* handles) {
+  if (!c || !handles || peer < 0 || peer >= c->part.nparts || peer >= 8)
+    return fail(c, BBWADG_ERR_INVALID_ARG, "bad arguments");
+  if (c->transport != 1) return fail(c, BBWADG_ERR_INVALID_ARG, "context was not set up with halo_transport 1");
+  if (peer == c->part.rank) return fail(c, BBWADG_ERR_INVALID_ARG, "a rank does not open its own handles");
+  if (c->peer_ipc[peer]) return BBWADG_OK;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  for (int b = 0; b < 2; ++b) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + 64 * b, 64);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      if (b == 1) cudaIpcCloseMemHandle(c->peer_q[peer][0]);
+      c->peer_q[peer][0] = nullptr;
+      return fail(c, BBWADG_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    c->peer_q[peer][b] = p;
+  }
+  c->peer_ipc[peer] = true;
+  return BBWADG_OK;
+}
+
 bbwadg_status bbwadg_step(bbwadg_ctx c, double t, double dt) {
   if (!c) return fail(c, BBWADG_ERR_INVALID_ARG, "null ctx");
   if (c->group) return fail(c, BBWADG_ERR_INVALID_ARG, "use bbwadg_group_step for group contexts");
+  if (c->transport == 1 && c->part.nparts > 1)
+    return fail(c, BBWADG_ERR_INVALID_ARG, "peer-read (IPC) contexts advance by bbwadg_stage with a barrier between stages");
   CUDA_TRY(c, cudaSetDevice(c->device));
   for (int s = 0; s < 5; ++s) {
     bbwadg_status st = full_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], RK_A[s], RK_B[s], dt, t + RK_C[s] * dt);
@@ -694,6 +772,28 @@ bbwadg_status bbwadg_step(bbwadg_ctx c, double t, double dt) {
 
 bbwadg_status bbwadg_group_step(bbwadg_ctx* ctxs, int n, double t, double dt) {
   if (!ctxs || n < 1) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad group");
+  if (ctxs[0]->transport == 1) {
+    // peer reads: every member reads the other members' Q_in in place; one shared stream orders stage s of
+    // all members after stage s-1 of all members
+    if (n > 8) return fail(ctxs[0], BBWADG_ERR_UNSUPPORTED, "peer-read halo: at most 8 partitions");
+    for (int s = 0; s < 5; ++s) {
+      for (int r = 0; r < n; ++r)
+        for (int q = 0; q < n; ++q)
+          for (int b = 0; b < 2; ++b) ctxs[r]->peer_q[q][b] = ctxs[q]->d_Q[b];
+      for (int r = 0; r < n; ++r) {
+        bbwadg_ctx c = ctxs[r];
+        bbwadg_status st = launch_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], 0, c->part.K_local, RK_A[s], RK_B[s],
+                                       dt, t + RK_C[s] * dt);
+        if (st) return st;
+      }
+      for (int r = 0; r < n; ++r) ctxs[r]->cur ^= 1;
+    }
+    for (int r = 0; r < n; ++r) {
+      ctxs[r]->steps++;
+      ctxs[r]->t = t + dt;
+    }
+    return BBWADG_OK;
+  }
   for (int s = 0; s < 5; ++s) {
     // pack all partitions, then copy every ghost block from its owner's send buffer
     for (int r = 0; r < n; ++r) {
@@ -830,8 +930,12 @@ void bbwadg_destroy(bbwadg_ctx c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int r = 0; r < 8; ++r)
+    if (c->peer_ipc[r])
+      for (int b = 0; b < 2; ++b)
+        if (c->peer_q[r][b]) cudaIpcCloseMemHandle(c->peer_q[r][b]);
   void* bufs[] = {c->d_tab, c->d_Q[0], c->d_Q[1], c->d_res, c->d_c2, c->d_geo, c->d_nbr, c->d_code,
-                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag, c->d_ptime};
+                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag, c->d_ptime, c->d_gmap};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm) nccl::comm_destroy(c->comm);

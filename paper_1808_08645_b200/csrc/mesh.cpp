@@ -225,6 +225,25 @@ Part build_part(const GlobalMesh& g, int rank, int nparts) {
       }
     }
   }
+  // owner-local index of every element in its own partition (the same interior-first, global-id order
+  // build_part gives that partition), for the peer-read transport's ghost map
+  std::vector<int32_t> lidx(g.K, -1);
+  {
+    std::vector<uint8_t> isb(g.K, 0);
+    for (int64_t k = 0; k < g.K; ++k)
+      for (int f = 0; f < 4; ++f) {
+        int64_t nb = g.etoe[4 * k + f];
+        if (nb >= 0 && g.owner[nb] != g.owner[k]) isb[k] = 1;
+      }
+    std::vector<int32_t> nint(nparts, 0), cnt(nparts, 0);
+    for (int64_t k = 0; k < g.K; ++k)
+      if (!isb[k]) ++nint[g.owner[k]];
+    for (int64_t k = 0; k < g.K; ++k)
+      if (!isb[k]) lidx[k] = cnt[g.owner[k]]++;
+    for (int r = 0; r < nparts; ++r) cnt[r] = nint[r];
+    for (int64_t k = 0; k < g.K; ++k)
+      if (isb[k]) lidx[k] = cnt[g.owner[k]]++;
+  }
   P.send_off.assign(nparts + 1, 0);
   P.recv_off.assign(nparts + 1, 0);
   for (int r = 0; r < nparts; ++r) {
@@ -237,6 +256,9 @@ Part build_part(const GlobalMesh& g, int rank, int nparts) {
     for (size_t j = 0; j < v.size(); ++j) {
       int64_t slot = P.recv_off[r] + (int64_t)j;
       P.nbr[4 * v[j].lk + v[j].f] = (int32_t)(-2 - slot);
+      const int64_t nbg = g.etoe[4 * P.gid[v[j].lk] + v[j].f];
+      P.gmap.push_back(r);
+      P.gmap.push_back(lidx[nbg]);
       P.send_faces.push_back(v[j].lk);
       P.send_faces.push_back(v[j].f);
     }

@@ -34,6 +34,7 @@ struct Part {
   std::vector<int32_t> send_faces;// [nsend][2] (local element, face), grouped by destination rank
   std::vector<int64_t> send_off;  // [nparts+1] face offsets per destination rank
   std::vector<int64_t> recv_off;  // [nparts+1] ghost-slot offsets per source rank
+  std::vector<int32_t> gmap;      // [nghost][2]: (owner rank, owner-local element id) of each ghost slot
   int64_t num_ghost() const { return recv_off.empty() ? 0 : recv_off.back(); }
 };
 

@@ -51,6 +51,13 @@ struct StageArgs {
   const int* nbr;      // [K][4]
   const uint8_t* code; // [K][4] = 6 f' + sigma
   const R* ghost;      // [slots][2][NFP]: p and u.n_sender at the sender's face nodes (halo, Eq. sdf)
+  // peer-read halo (halo_transport 1): the stage inputs Q_in of the other partitions (same device, or mapped
+  // from other processes / GPUs by CUDA IPC over NVLink), indexed by owner rank; gmap[slot] = (owner rank,
+  // owner-local element id) of ghost slot `slot`.  Partition faces then read the neighbour's traces directly
+  // (no pack, no collective) with the interior-face arithmetic, so partitioned runs are bitwise equal to
+  // the single-partition run.
+  const R* peer[8];
+  const int* gmap;
   const R* src;        // [K][NP] or null
   const uint8_t* tab;  // table blob (layout.hpp)
   long long elem_begin, elem_end;
@@ -1271,6 +1278,16 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
               tux[k][u] = __ldg(qn + NP);
               tuy[k][u] = __ldg(qn + 2 * NP);
               tuz[k][u] = __ldg(qn + 3 * NP);
+            } else if (nb < -1 && A.gmap) {
+              // partition face, peer-read transport: the owner's Q_in, read in place
+              const int slot = -2 - nb;
+              const int2 gm = __ldg(reinterpret_cast<const int2*>(A.gmap) + slot);
+              const int vol = __ldg(nbrvol + code * NFP + i);
+              const R* qn = A.peer[gm.x] + (long long)gm.y * 4 * NP + vol;
+              tpp[k][u] = __ldg(qn);
+              tux[k][u] = __ldg(qn + NP);
+              tuy[k][u] = __ldg(qn + 2 * NP);
+              tuz[k][u] = __ldg(qn + 3 * NP);
             } else if (nb < -1) {
               // partition face: the halo carries p+ and u+.n+ (n+ = the sender's outward normal = -n);
               // the flux needs only [[p]] and n.[[u]] (Eq. sdf); tux holds u+.n+
@@ -1338,7 +1355,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
           const char* gs = gb + u * EB + (C::O_GEO + 12 + 4 * f) * RB;
           const R nx = ld<R>(gs), ny = ld<R>(gs + RB), nz = ld<R>(gs + 2 * RB), sc = ld<R>(gs + 3 * RB) * cs;
           const R jp = pp - pm;
-          const R jun = (nb < -1) ? -tux[k][u] - (nx * uxm + ny * uym + nz * uzm)
+          const R jun = (nb < -1 && !A.gmap) ? -tux[k][u] - (nx * uxm + ny * uym + nz * uzm)
                                   : nx * (uxp - uxm) + ny * (uyp - uym) + nz * (uzp - uzm);
           if (act) {
             st<R>(gb + u * EB + (C::Y_F + (2 * f) * NFP + i) * RB, R(0.5) * sc * (A.tau_p * jp - jun));

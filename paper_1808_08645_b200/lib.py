@@ -27,7 +27,7 @@ class bbwadg_options(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("tau_p", ctypes.c_double), ("tau_u", ctypes.c_double),
                 ("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world_size", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
-                ("partition", ctypes.c_int * 3), ("check_c2", ctypes.c_int), ("reserved0", ctypes.c_int),
+                ("partition", ctypes.c_int * 3), ("check_c2", ctypes.c_int), ("halo_transport", ctypes.c_int),
                 ("c2_gids", ctypes.c_void_p), ("c2_rows", ctypes.c_int64), ("reserved", ctypes.c_int * 4)]
 
 
@@ -69,6 +69,9 @@ def _load() -> ctypes.CDLL:
         "bbwadg_rhs": (S, [ctx_p, V, D, V]),
         "bbwadg_wadg_apply": (S, [ctx_p, V, V]),
         "bbwadg_step": (S, [ctx_p, D, D]),
+        "bbwadg_stage": (S, [ctx_p, I, D, D]),
+        "bbwadg_ipc_get_handles": (S, [ctx_p, V]),
+        "bbwadg_ipc_open_peer": (S, [ctx_p, I, V]),
         "bbwadg_group_step": (S, [V, I, D, D]),
         "bbwadg_run": (S, [ctx_p, D, D, ctypes.c_int64]),
         "bbwadg_synchronize": (S, [ctx_p]),
@@ -165,6 +168,21 @@ def bbwadg_wadg_apply(ctx, r_dev, out_dev):
 
 def bbwadg_step(ctx, t: float, dt: float):
     _check(_L.bbwadg_step(ctx, float(t), float(dt)), ctx)
+
+
+def bbwadg_stage(ctx, s: int, t: float, dt: float):
+    _check(_L.bbwadg_stage(ctx, s, t, dt), ctx)
+
+
+def bbwadg_ipc_get_handles(ctx) -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_L.bbwadg_ipc_get_handles(ctx, buf), ctx)
+    return buf.raw
+
+
+def bbwadg_ipc_open_peer(ctx, peer: int, handles: bytes):
+    buf = ctypes.create_string_buffer(bytes(handles), 128)
+    _check(_L.bbwadg_ipc_open_peer(ctx, peer, buf), ctx)
 
 
 def bbwadg_group_step(ctxs, t: float, dt: float):

@@ -274,6 +274,69 @@ def test_group_partition_matches_single(gpu_lib, nparts, N, M):
     assert per_elem.max() <= 1e-13, per_elem.max()
 
 
+@pytest.mark.parametrize("nparts,N,M", [(2, 7, 4), (4, 3, 1), (8, 5, 3), (3, 2, 2)])
+def test_group_peer_read_halo_is_bitwise(gpu_lib, nparts, N, M):
+    """Peer-read halo (halo_transport 1): the stage kernel reads the owner partition's Q_in in place on
+    partition faces and forms the flux with the interior-face arithmetic, so P partitions reproduce the
+    single-partition run BITWISE (SURVEY §8(e) correctness criterion), N = 2, 3 with sub-warp groups."""
+    from paper_1808_08645_b200 import lib as L
+
+    v, e = kuhn.kuhn_mesh(4)
+    c2 = media.random_c2(len(e), M)
+    Q0 = states.random_state(len(e), N)
+    dt = 1e-3
+    single = _solver(v, e, N, M, c2)
+    single.set_state(Q0)
+    for i in range(3):
+        single.step(i * dt, dt)
+    ref = single.get_state()
+    o = L.bbwadg_default_options()
+    o.halo_transport = 1
+    ctxs = L.bbwadg_setup_group(v, e, N, M, c2, o, nparts)
+    gids = []
+    for c in ctxs:
+        info = L.bbwadg_query(c)
+        g = np.ctypeslib.as_array(info.global_ids, shape=(info.num_elements_local,)).copy()
+        gids.append(g)
+        L.bbwadg_set_state(c, np.ascontiguousarray(Q0[g]), 0)
+        assert info.num_halo_faces > 0
+    for i in range(3):
+        L.bbwadg_group_step(ctxs, i * dt, dt)
+    out = np.zeros_like(ref)
+    for c, g in zip(ctxs, gids):
+        loc = np.empty((len(g), 4, states.num_coeffs(N)))
+        L.bbwadg_get_state(c, loc, 0)
+        out[g] = loc
+    for c in ctxs:
+        L.bbwadg_destroy(c)
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_peer_read_halo_across_processes(gpu_lib, tmp_path, world):
+    """`world` processes (sharing the one GPU of the test box), one partition each, CUDA-IPC-mapped state
+    buffers, bbwadg_stage + barrier: the gathered state equals the single-process run bitwise."""
+    import subprocess
+    import sys
+
+    N, M, n, steps = 5, 3, 4, 3
+    outf = tmp_path / "ipc.npz"
+    port = 29533 + world
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(world),
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "scripts/ipc_halo_parity.py",
+                        str(outf), str(n), str(N), str(M), str(steps)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = np.load(outf)
+    assert np.all(d["halo"] > 0)
+    v, e = kuhn.kuhn_mesh(n)
+    c2 = media.random_c2(len(e), M)
+    single = _solver(v, e, N, M, c2)
+    single.set_state(states.random_state(len(e), N))
+    for i in range(steps):
+        single.step(i * 1e-3, 1e-3)
+    assert np.array_equal(d["Q"], single.get_state())
+
+
 # ------------------------------------------------------------------------------------ full sizes
 def _neighbour_closure(e, sample):
     """sample elements plus every element sharing a face with one of them (numpy face matching)."""

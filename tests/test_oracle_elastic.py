@@ -10,7 +10,7 @@ Each part of the elastic right-hand side is checked against something other than
 * the penalty fluxes: the semi-discrete energy rate equals minus the face integrals of
   tau_v/2 |A_n [[v]]|^2 + tau_s/2 |A_n^T [[sigma]]|^2 (interior) and tau_s |A_n^T sigma|^2 (traction-free
   boundary), computed here from physical face points; zero with tau = 0; doubled penalties fail it;
-* the time-discrete solution converges at rate ~N+1 to the exact standing P-wave (R26).
+* the time-discrete solution converges at rate ~N+1 to the exact standing P-wave (R27).
 """
 import numpy as np
 import pytest
@@ -244,7 +244,7 @@ def test_energy_non_increasing_in_time():
 
 @pytest.mark.slow
 def test_standing_p_wave_convergence_rate():
-    # exact standing P-wave (R26: lambda = 0, mu = 1/2, rho = 1, traction-free box)
+    # exact standing P-wave (R27: lambda = 0, mu = 1/2, rho = 1, traction-free box)
     N, M = 2, 1
     errs = []
     for n in [2, 4]:
