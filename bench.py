@@ -454,56 +454,82 @@ def elastic_runs(args, dev):
     return out
 
 
-def sweep(args, dev):
-    """BASELINE config 3: N = 1..9, M = N on the n=44 Kuhn mesh (511,104 tets), fp64."""
+def _time_row(v, e, n, N, M, c2, dev, warmup, steps):
+    """One acoustic (N, M) configuration on mesh (v, e): Gaussian pulse state, `warmup` + `steps` LSRK45
+    steps, clocks sampled during the timed steps."""
     import torch
 
     from paper_1808_08645_b200 import Solver
+
+    peaks, _ = load_peaks()
+    Np = comb(N + 3, 3)
+    s = Solver(v, e, N, M, c2, device=dev.index, stream=torch.cuda.current_stream(dev))
+    s.set_state(pulse_state(v, e, N, dev))
+    h_min = 2.0 / n / (1 + np.sqrt(2) + np.sqrt(3))
+    dt = 0.5 * h_min / (np.sqrt(1.5) * (N + 1) ** 2)
+    for i in range(warmup):
+        s.step(i * dt, dt)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        a.record()
+        for i in range(steps):
+            s.step((warmup + i) * dt, dt)
+        b.record()
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    info = s.info()
+    gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
+    row = {"N": N, "M": M, "value": 4.0 * len(e) * Np * 5 / (ms / 1e3), "ms_per_step": ms,
+           "ns_per_element_stage": ms * 1e6 / (5 * len(e)), "hbm_frac": gbs / peaks["hbm_gbs"],
+           "tflops": info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12,
+           "flops_per_element_stage": info["flops_per_stage"] / len(e),
+           "bytes_per_element_stage": info["algorithmic_bytes_per_stage"] / len(e),
+           "warmup": warmup, "steps": steps, "clocks": clk.summary()}
+    s.close()
+    return row
+
+
+def sweep(args, dev):
+    """BASELINE config 3: N = 1..9, M = N on the n=44 Kuhn mesh (511,104 tets), fp64; plus the paper's
+    fixed-M runtime study (BBWADG-1: M = 1, N = 1..9) and an M sweep at N = 7 (M = 0..7)
+    on the same mesh and media (c^2 k = 8)."""
     from workloads import kuhn, media
 
     v, e = kuhn.kuhn_mesh(args.sweep_n)
     f = media.c2_smooth(8.0)
-    peaks, _ = load_peaks()
-    rows = []
-    for N in range(1, 10):
-        M = N
-        Np = comb(N + 3, 3)
-        c2 = media.project_c2(v, e, f, M, device=dev)
-        s = Solver(v, e, N, M, c2, device=dev.index, stream=torch.cuda.current_stream(dev))
-        s.set_state(pulse_state(v, e, N, dev))
-        h_min = 2.0 / args.sweep_n / (1 + np.sqrt(2) + np.sqrt(3))
-        dt = 0.5 * h_min / (np.sqrt(1.5) * (N + 1) ** 2)
-        for i in range(args.sweep_warmup):
-            s.step(i * dt, dt)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        nst = args.sweep_steps
-        with ClockSampler(dev.index) as clk:
-            torch.cuda.synchronize()
-            a.record()
-            for i in range(nst):
-                s.step((args.sweep_warmup + i) * dt, dt)
-            b.record()
-            torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / nst
-        info = s.info()
-        gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
-        rows.append({"N": N, "M": M, "value": 4.0 * len(e) * Np * 5 / (ms / 1e3), "ms_per_step": ms,
-                     "ns_per_element_stage": ms * 1e6 / (5 * len(e)), "hbm_frac": gbs / peaks["hbm_gbs"],
-                     "tflops": info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12,
-                     "flops_per_element_stage": info["flops_per_stage"] / len(e),
-                     "bytes_per_element_stage": info["algorithmic_bytes_per_stage"] / len(e),
-                     "warmup": args.sweep_warmup, "steps": nst, "clocks": clk.summary()})
-        s.close()
-    sel = [r for r in rows if r["N"] >= 4]
-    Ns = np.log(np.array([r["N"] for r in sel], dtype=float))
-    fit = lambda y: float(np.polyfit(Ns, np.log(np.array(y, dtype=float)), 1)[0])
-    return {"workload": f"config3: Kuhn n={args.sweep_n} ({len(e):,} tets), M=N, c^2 k=8, Gaussian pulse "
-                        f"p = exp(-50|x|^2), u = 0, fp64; {args.sweep_warmup} warm-up + {args.sweep_steps} timed steps per N",
-            "rows": rows, "loglog_slope_time_per_element_N4to9": fit([r["ns_per_element_stage"] for r in sel]),
-            "loglog_slope_algorithmic_flops_N4to9": fit([r["flops_per_element_stage"] for r in sel]),
-            "loglog_slope_algorithmic_bytes_N4to9": fit([r["bytes_per_element_stage"] for r in sel]),
-            "paper_prediction": "O(N^4) per element for the WADG update at fixed M (P:1693); bytes O(N^3)"}
+    c2cache = {}
+
+    def c2_of(M):
+        if M not in c2cache:
+            c2cache[M] = media.project_c2(v, e, f, M, device=dev)
+        return c2cache[M]
+
+    def run(pairs):
+        return [_time_row(v, e, args.sweep_n, N, M, c2_of(M), dev, args.sweep_warmup, args.sweep_steps) for N, M in pairs]
+
+    def slope(rows, key):
+        sel = [r for r in rows if r["N"] >= 4]
+        Ns = np.log(np.array([r["N"] for r in sel], dtype=float))
+        return float(np.polyfit(Ns, np.log(np.array([r[key] for r in sel], dtype=float)), 1)[0])
+
+    rows = run([(N, N) for N in range(1, 10)])
+    out = {"workload": f"config3: Kuhn n={args.sweep_n} ({len(e):,} tets), M=N, c^2 k=8, Gaussian pulse "
+                       f"p = exp(-50|x|^2), u = 0, fp64; {args.sweep_warmup} warm-up + {args.sweep_steps} timed steps per N",
+           "rows": rows, "loglog_slope_time_per_element_N4to9": slope(rows, "ns_per_element_stage"),
+           "loglog_slope_algorithmic_flops_N4to9": slope(rows, "flops_per_element_stage"),
+           "loglog_slope_algorithmic_bytes_N4to9": slope(rows, "bytes_per_element_stage"),
+           "paper_prediction": "O(N^4) per element for the WADG update at fixed M (P:1693); bytes O(N^3)"}
+    if not args.no_msweep:
+        m1 = run([(N, 1) for N in range(1, 10)])
+        out["fixed_M1"] = {"rows": m1, "loglog_slope_time_per_element_N4to9": slope(m1, "ns_per_element_stage"),
+                           "loglog_slope_algorithmic_flops_N4to9": slope(m1, "flops_per_element_stage"),
+                           "note": "M = 1 (the paper's BBWADG-1): the generic row-convolution product is the "
+                                   "4-nonzero stencil of P:311-324 (3 row loads per output row)"}
+        out["M_sweep_N7"] = {"rows": run([(7, M) for M in (0, 1, 2, 3, 4, 5, 7)]),
+                             "note": "M = 0 takes the BBDG fast path (P:134: WADG = constant c^2)"}
+    return out
 
 
 def cpu_baseline(N, M, seconds, extras=False):
@@ -644,6 +670,7 @@ def main():
     ap.add_argument("--elastic", default="7:2:f64,7:2:f32,5:1:f64,3:1:f64,9:2:f64",
                     help="elastic BBWADG lines N:M:dtype (comma separated; '' skips them)")
     ap.add_argument("--elastic-n", type=int, default=56)
+    ap.add_argument("--no-msweep", action="store_true", help="skip the M=1 N-sweep and the N=7 M-sweep")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus != world and not (args.gpus == 1 and world == 1):
