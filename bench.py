@@ -340,6 +340,8 @@ def run_ours(args):
         out["config4"] = config4_runs(args, dev)
     if rank == 0 and args.elastic:
         out["elastic"] = elastic_runs(args, dev)
+    if rank == 0 and args.two_d:
+        out["two_d"] = runs_2d(args, dev)
     if rank == 0 and not args.no_sweep:
         out["sweep"] = sweep(args, dev)
     if rank == 0:
@@ -391,6 +393,59 @@ def config4_runs(args, dev):
         s.close()
     out["workload"] = (f"config4: Kuhn n={n} ({len(e):,} tets), N={N}, M={M}, layered c^2 1/1.5/2.25 (sub-cell "
                        f"jumps), Gaussian pulse")
+    return out
+
+
+def runs_2d(args, dev):
+    """2D triangles: [-1,1]^2 cut into n x n x 2 triangles (n = 512: 524,288
+    triangles; state 0.45 GB at N = 7, far above the L2), c^2 = 1 + 1/2 sin(pi x) sin(pi y) projected to P^M, Gaussian pulse; 3 warm-up + 10
+    timed steps per line, clocks sampled; value = 3 K Np2 5 steps / device time."""
+    import torch
+
+    from paper_1808_08645_b200 import Solver2D
+    from workloads import tri2d
+
+    n = args.n2d
+    v, e = tri2d.tri_mesh(n)
+    peaks, _ = load_peaks()
+    out = {"workload": f"2D: {n}x{n}x2 triangles ({len(e):,}), smooth c^2 (P:672), Gaussian pulse exp(-50|x|^2)"}
+    c2c, qc = {}, {}
+    for spec in args.two_d.split(","):
+        N, M, dt_name = spec.split(":")
+        N, M = int(N), int(M)
+        Np = (N + 1) * (N + 2) // 2
+        if M not in c2c:
+            c2c[M] = tri2d.project_c2(v, e, tri2d.c2_smooth_2d(1.0), M)
+        if N not in qc:
+            qc[N] = tri2d.gaussian_pulse(v, e, N)
+        c2, Q0 = c2c[M], qc[N]
+        s = Solver2D(v, e, N, M, c2, dtype=dt_name, device=dev.index, stream=torch.cuda.current_stream(dev))
+        s.set_state(Q0 if dt_name == "f64" else Q0.astype(np.float32))
+        dt = 0.5 * tri2d.min_height(v, e) / (np.sqrt(c2.max()) * (N + 1) ** 2)
+        for i in range(3):
+            s.step(i * dt, dt)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev.index) as clk:
+            torch.cuda.synchronize()
+            a.record()
+            for i in range(10):
+                s.step((3 + i) * dt, dt)
+            b.record()
+            torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        info = s.info()
+        gbs = info["algorithmic_bytes_per_stage"] / (ms / 5 / 1e3) / 1e9
+        out[f"N{N}M{M}{dt_name}"] = {
+            "value": 3.0 * len(e) * Np * 5 / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(gbs / peaks["hbm_gbs"], 4), "kernel": f"bbw::stage2d_kernel<N={N},M={M},{dt_name}>",
+                         "algorithmic_bytes_per_launch": info["algorithmic_bytes_per_stage"],
+                         "achieved_tflops": round(info["flops_per_stage"] / (ms / 5 / 1e3) / 1e12, 3)},
+            "warmup": 3, "steps": 10, "gpu_launches": 50, "clocks": clk.summary()}
+        s.close()
+        del s
+        torch.cuda.empty_cache()
     return out
 
 
@@ -670,6 +725,9 @@ def main():
     ap.add_argument("--elastic", default="7:2:f64,7:2:f32,5:1:f64,3:1:f64,9:2:f64",
                     help="elastic BBWADG lines N:M:dtype (comma separated; '' skips them)")
     ap.add_argument("--elastic-n", type=int, default=56)
+    ap.add_argument("--two-d", default="7:4:f64,7:4:f32,3:1:f64,9:2:f64",
+                    help="2D triangle lines N:M:dtype (comma separated; '' skips them)")
+    ap.add_argument("--n2d", type=int, default=512)
     ap.add_argument("--no-msweep", action="store_true", help="skip the M=1 N-sweep and the N=7 M-sweep")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

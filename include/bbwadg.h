@@ -188,6 +188,24 @@ bbwadg_status bbwadg_elastic_setup(const bbwadg_mesh* mesh, int N, int M, const 
                                    const double* lambda, const double* mu, const bbwadg_options* opts,
                                    bbwadg_ctx* out);
 
+/* ---- 2D triangles (2D experiments P:646-652): the acoustic
+ * BBWADG scheme on affine triangles (R29-R30), one fused kernel per RK stage.
+ *   mesh:  vertices [num_vertices][2], elements [K][3] global vertex ids, counter-clockwise (J > 0;
+ *          clockwise triangles are rejected, never reordered); edge f = the edge opposite local vertex f.
+ *   c2:    host [K][Mp2] degree-M Bernstein coefficients of c^2, Mp2 = (M+1)(M+2)/2, canonical order
+ *          for a2 in 0..M: for a1 in 0..M-a2 (a0 = M - a1 - a2).
+ * The context uses the common calls with 3 fields: state Q[K][3][Np2] = (p, u_x, u_y), Np2 =
+ * (N+1)(N+2)/2; bbwadg_set_source takes [K][Np2] (the 2D manufactured source of P:646-652);
+ * bbwadg_wadg_apply maps [K][Np2] -> [K][Np2].  world_size must be 1. */
+typedef struct {
+  int64_t num_vertices;
+  const double* vertices;   /* [num_vertices][2] */
+  int64_t num_elements;
+  const int64_t* elements;  /* [num_elements][3] */
+} bbwadg_mesh2d;
+bbwadg_status bbwadg2d_setup(const bbwadg_mesh2d* mesh, int N, int M, const double* c2_coeffs,
+                             const bbwadg_options* opts, bbwadg_ctx* out);
+
 /* ---- in-process partition groups (test/debug: P partitions on one device,
  * halo exchanged by device copies instead of NCCL; validates partitioning,
  * packing, orientation and the interior/boundary split without a cluster) */

@@ -13,7 +13,7 @@ test infrastructure and is never imported from here).
 """
 import importlib
 
-__all__ = ["lib", "Solver", "ElasticSolver", "build"]
+__all__ = ["lib", "Solver", "ElasticSolver", "Solver2D", "build"]
 
 
 def __getattr__(name):
@@ -21,6 +21,8 @@ def __getattr__(name):
         return importlib.import_module(".lib", __name__)
     if name == "Solver":
         return importlib.import_module(".solver", __name__).Solver
+    if name == "Solver2D":
+        return importlib.import_module(".solver", __name__).Solver2D
     if name == "ElasticSolver":
         return importlib.import_module(".solver", __name__).ElasticSolver
     if name == "build":

@@ -16,6 +16,8 @@
 #include "mesh.hpp"
 #include "nccl_shim.hpp"
 #include "elastic_kernel.cuh"
+#include "layout2d.hpp"
+#include "stage2d_kernel.cuh"
 #include "stage_kernel.cuh"
 #include "tables.hpp"
 #include "layout.hpp"
@@ -54,7 +56,8 @@ struct Group;
 
 struct bbwadg_ctx_s {
   int N = 0, M = 0, dtype = 0, device = 0, Np = 0, Mp = 0, Nfp = 0;
-  int nfields = 4;       // 4 acoustic (p, u), 9 elastic (v, sigma)
+  int nfields = 4;       // 4 acoustic (p, u), 9 elastic (v, sigma), 3 for 2D (p, u_x, u_y)
+  int dim = 3;           // 2: triangle context (bbwadg2d_setup, NEXT-4)
   bool elastic = false;  // bbwadg_elastic_setup context (NEXT-2)
   size_t rb = 8;  // bytes per real
   double tau_p = 1, tau_u = 1;
@@ -175,11 +178,50 @@ bbwadg_status launch_elastic_pass(bbwadg_ctx c, int mode, const void* Qin, void*
                                 : launch_elastic_typed<float>(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt, grid);
 }
 
+// 2D (triangle) stage kernel over local elements [b, e) (Q: [K][3][Np2]).
+template <typename R>
+bbwadg_status launch_2d_typed(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e, double rk_a,
+                              double rk_b, double dt, double tstage, int grid) {
+  Stage2DArgs<R> a;
+  std::memset(&a, 0, sizeof(a));
+  a.Qin = static_cast<const R*>(Qin);
+  a.Qout = static_cast<R*>(Qout);
+  a.res = static_cast<R*>(c->d_res);
+  a.c2 = static_cast<const R*>(c->d_c2);
+  a.geo = static_cast<const R*>(c->d_geo);
+  a.nbr = c->d_nbr;
+  a.code = c->d_code;
+  a.src = static_cast<const R*>(c->d_src);
+  a.tab = static_cast<const uint8_t*>(c->d_tab);
+  a.elem_begin = b;
+  a.elem_end = e;
+  a.rk_a = (R)rk_a;
+  a.rk_b = (R)rk_b;
+  a.dt = (R)dt;
+  a.src_amp = (R)std::sin(M_PI * tstage);
+  a.tau_p = (R)c->tau_p;
+  a.tau_u = (R)c->tau_u;
+  for (int j = 0; j < 10; ++j) a.gam[j] = (R)c->tables.gam[j];
+  a.mode = mode;
+  cudaError_t err = c->ks.launch_stage(&a, grid, c->stream);
+  if (err != cudaSuccess) return fail(c, BBWADG_ERR_CUDA, std::string("2D kernel launch: ") + cudaGetErrorString(err));
+  return BBWADG_OK;
+}
+
+bbwadg_status launch_2d_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e, double rk_a,
+                             double rk_b, double dt, double tstage) {
+  const int64_t nb = (e - b + c->ks.elems_per_cta - 1) / c->ks.elems_per_cta;
+  const int grid = (int)std::min<int64_t>(nb, c->grid);
+  return c->dtype == BBWADG_F64 ? launch_2d_typed<double>(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt, tstage, grid)
+                                : launch_2d_typed<float>(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt, tstage, grid);
+}
+
 // Launch one kernel pass over local elements [b, e).
 bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, int64_t b, int64_t e, double rk_a,
                           double rk_b, double dt, double tstage, int grid_cap = 0) {
   if (e <= b) return BBWADG_OK;
   if (c->elastic) return launch_elastic_pass(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt);
+  if (c->dim == 2) return launch_2d_pass(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt, tstage);
   int64_t nb = (e - b + c->ks.elems_per_cta - 1) / c->ks.elems_per_cta;
   int grid = (int)std::min<int64_t>(nb, grid_cap > 0 ? grid_cap : c->grid);
   cudaError_t err;
@@ -620,6 +662,177 @@ bbwadg_status bbwadg_elastic_setup(const bbwadg_mesh* mesh, int N, int M, const 
   return setup_one(g, N, M, mat.data(), o, 0, 1, nullptr, out, true);
 }
 
+bbwadg_status bbwadg2d_setup(const bbwadg_mesh2d* mesh, int N, int M, const double* c2, const bbwadg_options* opts,
+                             bbwadg_ctx* out) {
+  if (!out) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  bbwadg_options o;
+  bbwadg_default_options(&o);
+  if (opts) o = *opts;
+  if (!mesh || !mesh->vertices || !mesh->elements || mesh->num_elements < 1 || mesh->num_vertices < 3 || !c2)
+    return fail(nullptr, BBWADG_ERR_INVALID_ARG, "mesh/c2 pointers or sizes invalid");
+  if (N < 1 || N > BBWADG_MAX_N || M < 0 || M > N)
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "need 1 <= N <= 9 and 0 <= M <= N");
+  if (o.dtype != BBWADG_F64 && o.dtype != BBWADG_F32)
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "dtype must be BBWADG_F64 or BBWADG_F32");
+  if (o.tau_p < 0 || o.tau_u < 0) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "tau must be >= 0");
+  if (o.world_size != 1 || o.rank != 0 || o.c2_gids)
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "2D contexts run on one GPU (world_size 1, no c2_gids)");
+  const int64_t K = mesh->num_elements, nv = mesh->num_vertices;
+  const double* V = mesh->vertices;
+  const int64_t* E = mesh->elements;
+  // host mesh processing: orientation, edge connectivity by global vertex pairs, gradients, codes
+  static const int EV[3][2] = {{1, 2}, {0, 2}, {0, 1}};
+  std::vector<double> geo(6 * K);
+  std::vector<int32_t> nbr(3 * K, -1);
+  std::vector<uint8_t> code(3 * K, 0);
+  std::vector<std::pair<std::pair<int64_t, int64_t>, int64_t>> keys;  // ((min, max), 3 k + f)
+  keys.reserve(3 * K);
+  for (int64_t k = 0; k < K; ++k) {
+    int64_t g[3];
+    for (int i = 0; i < 3; ++i) {
+      g[i] = E[3 * k + i];
+      if (g[i] < 0 || g[i] >= nv) return fail(nullptr, BBWADG_ERR_MESH, "vertex id out of range");
+    }
+    const double ax = V[2 * g[1]] - V[2 * g[0]], ay = V[2 * g[1] + 1] - V[2 * g[0] + 1];
+    const double bx = V[2 * g[2]] - V[2 * g[0]], by = V[2 * g[2] + 1] - V[2 * g[0] + 1];
+    const double det = ax * by - ay * bx;
+    if (!(det > 0)) {
+      std::ostringstream os;
+      os << "triangle " << k << " is not positively oriented (det " << det << ")";
+      return fail(nullptr, BBWADG_ERR_MESH, os.str());
+    }
+    // l1, l2 = inverse of [a b]; grad l0 = -(grad l1 + grad l2)
+    const double g1x = by / det, g1y = -bx / det, g2x = -ay / det, g2y = ax / det;
+    double* gg = &geo[6 * k];
+    gg[0] = -(g1x + g2x);
+    gg[1] = -(g1y + g2y);
+    gg[2] = g1x;
+    gg[3] = g1y;
+    gg[4] = g2x;
+    gg[5] = g2y;
+    for (int f = 0; f < 3; ++f) {
+      const int64_t u = g[EV[f][0]], w = g[EV[f][1]];
+      keys.push_back({{std::min(u, w), std::max(u, w)}, 3 * k + f});
+    }
+  }
+  std::sort(keys.begin(), keys.end());
+  for (size_t i = 0; i < keys.size();) {
+    size_t j = i;
+    while (j < keys.size() && keys[j].first == keys[i].first) ++j;
+    if (j - i > 2) return fail(nullptr, BBWADG_ERR_MESH, "edge shared by more than two triangles");
+    if (j - i == 2) {
+      const int64_t s0 = keys[i].second, s1 = keys[i + 1].second;
+      const int64_t k0 = s0 / 3, k1 = s1 / 3;
+      const int f0 = (int)(s0 % 3), f1 = (int)(s1 % 3);
+      const int flip = E[3 * k0 + EV[f0][0]] != E[3 * k1 + EV[f1][0]];  // edges run opposite ways
+      nbr[3 * k0 + f0] = (int32_t)k1;
+      nbr[3 * k1 + f1] = (int32_t)k0;
+      code[3 * k0 + f0] = (uint8_t)(2 * f1 + flip);
+      code[3 * k1 + f1] = (uint8_t)(2 * f0 + flip);
+    }
+    i = j;
+  }
+  // c^2_M > 0: coefficients positive (convex hull), else sampled on the degree-(M+2) lattice
+  const int Mp = (M + 1) * (M + 2) / 2;
+  if (o.check_c2) {
+    const int qd = M + 2;
+    for (int64_t k = 0; k < K; ++k) {
+      const double* ck = c2 + (size_t)k * Mp;
+      bool allpos = true;
+      for (int b = 0; b < Mp; ++b) allpos = allpos && ck[b] > 0;
+      if (allpos) continue;
+      for (int p2 = 0; p2 <= qd; ++p2)
+        for (int p1 = 0; p1 <= qd - p2; ++p1) {
+          const double l[3] = {(double)(qd - p1 - p2) / qd, (double)p1 / qd, (double)p2 / qd};
+          double v = 0;
+          int bi = 0;
+          for (int b2 = 0; b2 <= M; ++b2)
+            for (int b1 = 0; b1 <= M - b2; ++b1, ++bi) {
+              const int b0 = M - b1 - b2;
+              double mult = 1;
+              for (int t = 2; t <= M; ++t) mult *= t;
+              for (int t = 2; t <= b0; ++t) mult /= t;
+              for (int t = 2; t <= b1; ++t) mult /= t;
+              for (int t = 2; t <= b2; ++t) mult /= t;
+              v += ck[bi] * mult * std::pow(l[0], b0) * std::pow(l[1], b1) * std::pow(l[2], b2);
+            }
+          if (!(v > 0)) {
+            std::ostringstream os;
+            os << "c^2_M is not positive in element " << k << " (sampled value " << v << ")";
+            return fail(nullptr, BBWADG_ERR_NONPOSITIVE_C2, os.str());
+          }
+        }
+    }
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) return fail(nullptr, BBWADG_ERR_NO_DEVICE, "no CUDA device");
+  std::unique_ptr<bbwadg_ctx_s> c(new bbwadg_ctx_s());
+  struct Cleanup {
+    std::unique_ptr<bbwadg_ctx_s>& p;
+    ~Cleanup() {
+      if (p) bbwadg_destroy(p.release());
+    }
+  } cleanup{c};
+  c->N = N;
+  c->M = M;
+  c->dim = 2;
+  c->nfields = 3;
+  c->dtype = o.dtype;
+  c->device = o.device;
+  c->rb = o.dtype == BBWADG_F64 ? 8 : 4;
+  c->tau_p = o.tau_p;
+  c->tau_u = o.tau_u;
+  c->Np = (N + 1) * (N + 2) / 2;
+  c->Mp = Mp;
+  c->Nfp = N + 1;
+  c->K_global = K;
+  CUDA_TRY(c.get(), cudaSetDevice(o.device));
+  c->ks = N <= 3 ? get_kernels2d_a(N, M, o.dtype) : N <= 6 ? get_kernels2d_b(N, M, o.dtype) : get_kernels2d_c(N, M, o.dtype);
+  if (!c->ks.launch_stage) return fail(nullptr, BBWADG_ERR_UNSUPPORTED, "no 2D kernel instantiation for this (N, M, dtype)");
+  CUDA_TRY(c.get(), c->ks.prepare());
+  int nsm = 0;
+  CUDA_TRY(c.get(), cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o.device));
+  c->grid = nsm * c->ks.blocks_per_sm();
+  c->stream = static_cast<cudaStream_t>(o.cuda_stream);
+  Part& P = c->part;
+  P.rank = 0;
+  P.nparts = 1;
+  P.K_local = K;
+  P.n_interior = K;
+  P.gid.resize(K);
+  for (int64_t i = 0; i < K; ++i) P.gid[i] = i;
+  P.nbr = nbr;
+  P.code = code;
+  P.send_off.assign(2, 0);
+  P.recv_off.assign(2, 0);
+  try {
+    c->tables = build_tables_2d(N, M, (int)c->rb);
+  } catch (const std::exception& ex) {
+    return fail(nullptr, BBWADG_ERR_UNSUPPORTED, ex.what());
+  }
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_tab, c->tables.blob.size()));
+  CUDA_TRY(c.get(), cudaMemcpy(c->d_tab, c->tables.blob.data(), c->tables.blob.size(), cudaMemcpyHostToDevice));
+  bbwadg_status st;
+  if ((st = upload_real(c.get(), &c->d_geo, geo))) return fail(nullptr, st, c->err);
+  if ((st = upload_real(c.get(), &c->d_c2, std::vector<double>(c2, c2 + (size_t)K * Mp)))) return fail(nullptr, st, c->err);
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_nbr, sizeof(int) * 3 * K));
+  CUDA_TRY(c.get(), cudaMemcpy(c->d_nbr, nbr.data(), sizeof(int) * 3 * K, cudaMemcpyHostToDevice));
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_code, 3 * K));
+  CUDA_TRY(c.get(), cudaMemcpy(c->d_code, code.data(), 3 * K, cudaMemcpyHostToDevice));
+  const size_t sb = state_bytes(c.get());
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(c.get(), cudaMalloc(&c->d_Q[b], std::max<size_t>(sb, 16)));
+    CUDA_TRY(c.get(), cudaMemset(c->d_Q[b], 0, sb));
+  }
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_res, std::max<size_t>(sb, 16)));
+  CUDA_TRY(c.get(), cudaMemset(c->d_res, 0, sb));
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_flag, sizeof(int)));
+  CUDA_TRY(c.get(), cudaDeviceSynchronize());
+  *out = c.release();
+  return BBWADG_OK;
+}
+
 bbwadg_status bbwadg_setup_group(const bbwadg_mesh* mesh, int N, int M, const double* c2_coeffs,
                                  const bbwadg_options* opts, int nparts, bbwadg_ctx* out) {
   if (!out || nparts < 1) return fail(nullptr, BBWADG_ERR_INVALID_ARG, "bad group arguments");
@@ -842,7 +1055,7 @@ bbwadg_status bbwadg_run(bbwadg_ctx c, double t0, double dt, int64_t nsteps) {
     if (s) return s;
   }
   CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
-  long long n = (long long)c->part.K_local * 4 * c->Np;
+  long long n = (long long)c->part.K_local * c->nfields * c->Np;
   if (n > 0) {
     if (c->dtype == BBWADG_F64)
       nonfinite_kernel<double><<<592, 256, 0, c->stream>>>(static_cast<const double*>(c->d_Q[c->cur]), n, c->d_flag);
@@ -897,7 +1110,8 @@ bbwadg_status bbwadg_query(bbwadg_ctx c, bbwadg_info* info) {
   // minimum HBM traffic of one fused stage: Q_in, res (read) + Q_out, res (write) = 16 Np words,
   // c^2_M (Mp words), geometry (12 words), connectivity (4 int32 + 4 bytes) per element.
   const double per_elem = c->elastic ? (36.0 * c->Np + 3.0 * c->Mp + 12.0) * c->rb + 20.0
-                                     : (16.0 * c->Np + c->Mp + 12.0) * c->rb + 20.0;
+                         : c->dim == 2 ? (12.0 * c->Np + c->Mp + 6.0) * c->rb + 15.0
+                                       : (16.0 * c->Np + c->Mp + 12.0) * c->rb + 20.0;
   info->algorithmic_bytes_per_stage = per_elem * P.K_local;
   const int N = c->N, M = c->M, Np = c->Np, Nfp = c->Nfp;
   double vol = 24.0 * np3(N - 1) + 8.0 * Np * 4;                  // gradient (24 flop/b) + elevation (8 flop/out)
@@ -907,6 +1121,18 @@ bbwadg_status bbwadg_query(bbwadg_ctx c, bbwadg_info* info) {
   for (int n = N + 1; n <= N + M; ++n) proj += 8.0 * np3(n - 1);
   for (int n = 1; n <= N; ++n) proj += 8.0 * np3(n - 1) + 10.0 * np3(n);
   double lsrk = 4.0 * 4 * Np;
+  if (c->dim == 2) {
+    // 2D: gradient 3 x 3 x 2 flop per degree-(N-1) coefficient + elevation; fluxes, 6 edge lifts (N layers of
+    // 2-point sums); product 2 Np Mp; projection 6 flop per reduction output, 8 per upward output; LSRK
+    const int Nfp2 = N + 1;
+    vol = 18.0 * (N * (N + 1) / 2) + 3.0 * 3 * Np;
+    surf = 3.0 * (Nfp2 * 20.0) + 6.0 * (3.0 * Nfp2 + 3.0 * Np);
+    mult = 2.0 * Np * c->Mp;
+    proj = 0;
+    for (int n = N + 1; n <= N + M; ++n) proj += 3.0 * (n * (n + 1) / 2);
+    for (int n = 1; n <= N; ++n) proj += 3.0 * (n * (n + 1) / 2) + 5.0 * ((n + 1) * (n + 2) / 2);
+    lsrk = 4.0 * 3 * Np;
+  }
   if (c->elastic) {
     // 9-field gradient (144 flop per degree-(N-1) coefficient) + 9 elevations; fluxes (~90 flop per face
     // node) + three 8-array lifts; ten scalar WADG applications; LSRK on 9 fields

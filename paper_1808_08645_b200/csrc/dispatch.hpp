@@ -22,6 +22,10 @@ struct KernelSet {
 };
 
 KernelSet get_kernels(int N, int M, int dtype);
+// 2D (triangle) stage kernels (launch_stage takes Stage2DArgs<R>); N = 1..3 / 4..6 / 7..9
+KernelSet get_kernels2d_a(int N, int M, int dtype);
+KernelSet get_kernels2d_b(int N, int M, int dtype);
+KernelSet get_kernels2d_c(int N, int M, int dtype);
 
 #define BBW_DECLARE_N(n) KernelSet get_kernels_N##n(int M, int dtype);
 BBW_DECLARE_N(1)

@@ -1041,13 +1041,16 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
   const long long nelem = A.elem_end - A.elem_begin;
   const long long nbatch = (nelem + ET - 1) / ET;
 #define BBW_PA(k) (q + TG * (k))
-#if BBW_TMA && BBW_CPASYNC
+  // TMA bulk staging for groups of >= 8 lanes (N >= 3); the 4-lane groups of N <= 2 stage with cp.async
+  // (TMA measured 0 % faster at (7,4); compute-sanitizer racecheck flags the TMA path only for 4-lane groups)
+  constexpr bool kTMA = BBW_TMA && BBW_CPASYNC && (TG >= 8);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + C::G * C::GB) + grp;
   unsigned mbar_phase = 0;
-  if (q == 0) mbar_init(mbar, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-#endif
+  if constexpr (kTMA) {
+    if (q == 0) mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+  }
 #if BBW_LSRK_TMEM
   static_assert(ET == 1 && BBW_LSRK_REG, "TMEM LSRK state: one element per batch, register-resident state model");
   // LSRK state columns: residual at [0, TMW), Q_in copy at [TMW, 2 TMW); TMW = 4 KO reals in 32-bit words,
@@ -1120,7 +1123,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
       constexpr int NV = 4 * NP / VEC;  // 16-B chunks of Q
       constexpr int GV = 12 * RB / 16;  // 16-B chunks of grad(lambda)
       const char* gq = reinterpret_cast<const char*>(A.Qin + k0 * 4 * NP);
-#if BBW_TMA
+      if constexpr (kTMA) {
       // one elected lane per group: Q block (4 Np reals), grad(lambda) (12 reals) and the 4 neighbour ids of
       // every element of the batch by TMA bulk copies on the group's mbarrier (no LSU wavefronts)
       (void)NV;
@@ -1135,7 +1138,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         }
       }
       for (int u = q; u < nE; u += TG) cp_async4(gb + u * EB + 28 * RB + 16, A.code + (k0 + u) * 4);  // 4 codes
-#else
+      } else {
 #pragma unroll
       for (int t0 = 0; t0 < ET * NV; t0 += TG) {
         const int t = t0 + q;
@@ -1151,7 +1154,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         else if (w == GV) cp_async16(eb + 28 * RB, A.nbr + (k0 + u) * 4);     // 4 neighbour ids
         else cp_async4(eb + 28 * RB + 16, A.code + (k0 + u) * 4);             // 4 codes (bytes)
       }
-#endif
+      }
       for (int t = q; t < nE * MP; t += TG) {
         const int u = t / MP, b = t - u * MP;
         cp_async_real<R>(gb + u * EB + (C::O_C + b) * RB, A.c2 + (k0 + u) * MP + b);
@@ -1173,12 +1176,10 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
       }
 #endif
       cp_async_wait_all();
-#if BBW_TMA
-      if (nE > 0) {
+      if (kTMA && nE > 0) {
         mbar_wait(mbar, mbar_phase);
         mbar_phase ^= 1;
       }
-#endif
       sync();
       for (int t = q; t < nE * 4; t += TG) {  // outward normal, |grad lambda_f|
         const int u = t >> 2, f = t & 3;
@@ -1632,9 +1633,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
         }
       }
     }
-#if BBW_TMA && BBW_CPASYNC
-    fence_proxy_async();  // this batch's generic smem accesses before the next batch's bulk (async-proxy) writes
-#endif
+    if constexpr (kTMA) fence_proxy_async();  // this batch's generic smem accesses before the next batch's bulk writes
     sync();
     BBW_PT(10);
   }

@@ -73,5 +73,8 @@ std::vector<double> mass_inverse_constants(int N);
 
 // Build every table for (N, M); RB = sizeof(real) of the device path.
 HostTables build_tables(int N, int M, int RB);
+// 2D (triangle) path (layout2d.hpp; R29-R30): tables and projection constants with d = 2.
+HostTables build_tables_2d(int N, int M, int RB);
+std::vector<double> projection_constants_2d(int N, int M);
 
 }  // namespace bbw

@@ -23,6 +23,11 @@ class bbwadg_mesh(ctypes.Structure):
                 ("num_elements", ctypes.c_int64), ("elements", ctypes.c_void_p)]
 
 
+class bbwadg_mesh2d(ctypes.Structure):
+    _fields_ = [("num_vertices", ctypes.c_int64), ("vertices", ctypes.c_void_p),
+                ("num_elements", ctypes.c_int64), ("elements", ctypes.c_void_p)]
+
+
 class bbwadg_options(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("tau_p", ctypes.c_double), ("tau_u", ctypes.c_double),
                 ("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p), ("rank", ctypes.c_int),
@@ -63,6 +68,7 @@ def _load() -> ctypes.CDLL:
         "bbwadg_setup": (S, [P(bbwadg_mesh), I, I, V, P(bbwadg_options), P(ctx_p)]),
         "bbwadg_setup_group": (S, [P(bbwadg_mesh), I, I, V, P(bbwadg_options), I, V]),
         "bbwadg_elastic_setup": (S, [P(bbwadg_mesh), I, I, V, V, V, P(bbwadg_options), P(ctx_p)]),
+        "bbwadg2d_setup": (S, [P(bbwadg_mesh2d), I, I, V, P(bbwadg_options), P(ctx_p)]),
         "bbwadg_set_state": (S, [ctx_p, V, I]),
         "bbwadg_get_state": (S, [ctx_p, V, I]),
         "bbwadg_set_source": (S, [ctx_p, V]),
@@ -136,6 +142,13 @@ def bbwadg_elastic_setup(vertices, elements, N: int, M: int, rho_inv, lam, mu, o
     ctx = ctypes.c_void_p()
     _check(_L.bbwadg_elastic_setup(ctypes.byref(m), N, M, _ptr(rho_inv), _ptr(lam), _ptr(mu), ctypes.byref(opts),
                                    ctypes.byref(ctx)))
+    return ctx
+
+
+def bbwadg2d_setup(vertices, elements, N: int, M: int, c2, opts: bbwadg_options):
+    m = bbwadg_mesh2d(vertices.shape[0], _ptr(vertices), elements.shape[0], _ptr(elements))
+    ctx = ctypes.c_void_p()
+    _check(_L.bbwadg2d_setup(ctypes.byref(m), N, M, _ptr(c2), ctypes.byref(opts), ctypes.byref(ctx)))
     return ctx
 
 

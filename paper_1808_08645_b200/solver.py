@@ -117,7 +117,7 @@ class Solver:
         return out
 
     def wadg_apply(self, r_dev):
-        shape = (self.K_local, self.Np) if self.NF == 4 else (self.K_local, self.NF, self.Np)
+        shape = (self.K_local, self.NF, self.Np) if self.NF == 9 else (self.K_local, self.Np)
         r_dev = self._check_dev(r_dev, shape, "r")
         out = self.torch.empty(r_dev.shape, dtype=self.tdtype, device=self.device)
         L.bbwadg_wadg_apply(self.ctx, r_dev, out)
@@ -184,6 +184,43 @@ class ElasticSolver(Solver):
         self.stream = stream
         o.check_c2 = 1 if check else 0
         self.ctx = L.bbwadg_elastic_setup(self._v, self._e, self.N, self.M, *mats, o)
+        info = self.info()
+        self.K_local = info["num_elements_local"]
+        self.global_ids = info["global_ids"]
+
+
+class Solver2D(Solver):
+    """2D (triangle) acoustic BBWADG through bbwadg2d_setup: vertices [nv, 2],
+    triangles [K, 3] counter-clockwise, c2 [K, Np2(M)], state [K, 3, Np2] = (p, u_x, u_y).  Single GPU."""
+
+    NF = 3
+
+    def __init__(self, vertices, elements, N: int, M: int, c2, *, dtype: str = "f64", tau_p: float = 1.0,
+                 tau_u: float = 1.0, device: int = 0, stream=None, check_c2: bool = True):
+        import torch
+
+        self.torch = torch
+        self.N, self.M = int(N), int(M)
+        self.Np, self.Mp = (N + 1) * (N + 2) // 2, (M + 1) * (M + 2) // 2
+        self.dtype = dtype
+        self.tdtype = torch.float64 if dtype == "f64" else torch.float32
+        self.device = torch.device("cuda", device)
+        self._v = np.ascontiguousarray(vertices, dtype=np.float64)
+        self._e = np.ascontiguousarray(elements, dtype=np.int64)
+        c2 = np.ascontiguousarray(c2, dtype=np.float64)
+        if self._v.ndim != 2 or self._v.shape[1] != 2 or self._e.ndim != 2 or self._e.shape[1] != 3:
+            raise ValueError("2D mesh: vertices [nv, 2], triangles [K, 3]")
+        if c2.shape != (self._e.shape[0], self.Mp):
+            raise ValueError(f"c2 must have shape [K, {self.Mp}]")
+        o = L.bbwadg_default_options()
+        o.dtype = L.BBWADG_F64 if dtype == "f64" else L.BBWADG_F32
+        o.tau_p, o.tau_u, o.device = float(tau_p), float(tau_u), int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        o.cuda_stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        self.stream = stream
+        o.check_c2 = 1 if check_c2 else 0
+        self.ctx = L.bbwadg2d_setup(self._v, self._e, self.N, self.M, c2, o)
         info = self.info()
         self.K_local = info["num_elements_local"]
         self.global_ids = info["global_ids"]

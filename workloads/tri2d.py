@@ -97,9 +97,12 @@ def _fit_op(n, q):
 def l2_fit(vertices, elements, func, degree: int, extra: int = 4) -> np.ndarray:
     """Bernstein coefficients [K, Np2(degree)] of the per-element L2 projection of func(x, y)."""
     lam, P = _fit_op(degree, degree + extra)
-    X = vertices[elements]  # K,3,2
-    pts = np.einsum("qv,kvd->kqd", lam, X)
-    return func(pts[..., 0], pts[..., 1]) @ P.T
+    out = np.empty((len(elements), P.shape[0]))
+    for s in range(0, len(elements), 65536):
+        X = vertices[elements[s:s + 65536]]  # c,3,2
+        pts = np.einsum("qv,kvd->kqd", lam, X)
+        out[s:s + 65536] = func(pts[..., 0], pts[..., 1]) @ P.T
+    return out
 
 
 def c2_smooth_2d(k: float = 1.0):
