@@ -265,6 +265,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 #ifndef BBW_TMA
 #define BBW_TMA 1  // element Q blocks, geometry and neighbour ids by cp.async.bulk (needs BBW_CPASYNC)
 #endif
+#ifndef BBW_TMA_MIN_TG
+#define BBW_TMA_MIN_TG 32  // TMA only for whole-warp groups (sub-warp groups: cp.async; see the kernel)
+#endif
 
 // predicated 16-B shared load into x[0..VEC): registers keep their old values when !p
 template <typename R, int OFF>
@@ -1041,9 +1044,9 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
   const long long nelem = A.elem_end - A.elem_begin;
   const long long nbatch = (nelem + ET - 1) / ET;
 #define BBW_PA(k) (q + TG * (k))
-  // TMA bulk staging for groups of >= 8 lanes (N >= 3); the 4-lane groups of N <= 2 stage with cp.async
-  // (TMA measured 0 % faster at (7,4); compute-sanitizer racecheck flags the TMA path only for 4-lane groups)
-  constexpr bool kTMA = BBW_TMA && BBW_CPASYNC && (TG >= 8);
+  // TMA bulk staging for whole-warp groups (N >= 5); the sub-warp groups of N <= 4 stage with cp.async
+  // (TMA measured 0 % faster at (7,4); compute-sanitizer racecheck flags the TMA path only for sub-warp groups)
+  constexpr bool kTMA = BBW_TMA && BBW_CPASYNC && (TG >= BBW_TMA_MIN_TG);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem_raw + C::G * C::GB) + grp;
   unsigned mbar_phase = 0;
   if constexpr (kTMA) {
