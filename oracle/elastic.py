@@ -18,14 +18,14 @@ and the matrix-weighted WADG update of Eq. ewadg:
     dSigma/dt = (I x M^-1) M_C r_sigma           -> (dSigma/dt)_s = sum_t P_q diag(C_st(x_q)) V_q r_{sigma,t}
 (M_{C} is the block matrix of scalar weighted mass matrices M_{C_st}; each block applied
 by the quadrature form of Eq. pwadg, exact for the degree-M polynomial weights).
-Boundary faces (R24): traction-free mirror sigma+ = -sigma, v+ = v (the elastic analogue
+Boundary faces (R26): traction-free mirror sigma+ = -sigma, v+ = v (the elastic analogue
 of the acoustic pressure-release R11; with it {{A_n^T sigma}} = 0 on the boundary).
 Material inputs (R25): per-element degree-M Bernstein coefficients of rho^-1, lambda, mu.
 
 Pins: tests/test_oracle_elastic.py (linear-field exactness of the volume terms, constant-weight WADG
 = C r, the mu = 0 / rho = 1 reduction to the (pinned) acoustic oracle, the energy-rate identity with
 the penalty face integrals, energy conservation with tau = 0, and the convergence rate on the exact
-standing P-wave of DESIGN.md R26).
+standing P-wave of DESIGN.md R27).
 """
 from __future__ import annotations
 

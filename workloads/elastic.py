@@ -10,7 +10,7 @@ coefficients of rho^-1, lambda and mu (R25), arrays [K][Np(M)].
   1/2 + 1/4 sin(k pi x)...  (the acoustic c^2 model of P:674 carried over to the Lame fields; the paper's
   elastic runs print no media -- DESIGN.md R25), L2-projected onto P^M.
 * random_state: standard normal coefficients, default_rng(1809).
-* standing_p_wave: the exact solution of DESIGN.md R26 (lambda = 0, mu = 1/2, rho = 1):
+* standing_p_wave: the exact solution of DESIGN.md R27 (lambda = 0, mu = 1/2, rho = 1):
       v_i = cos(pi x_i) cos(pi t),  s_ii = -sin(pi x_i) sin(pi t),  shear stresses 0,
   traction-free on the faces of [-1,1]^3.
 """
