@@ -129,3 +129,34 @@ def test_setup_validates_arguments_before_device(L):
         L.bbwadg_setup(v, e, 10, 1, np.ones((1, 4)), L.bbwadg_default_options())
     with pytest.raises(L.BBWADGError, match="UNSUPPORTED"):  # M > N
         L.bbwadg_setup(v, e, 2, 3, np.ones((1, 20)), L.bbwadg_default_options())
+
+
+def test_elastic_and_2d_setups_validate_before_device(L):
+    # bbwadg_elastic_setup / bbwadg2d_setup check arguments and the mesh on the host before any device call
+    from workloads import kuhn, tri2d
+
+    v, e = kuhn.kuhn_mesh(1)
+    K = len(e)
+    ones = np.ones((K, 4))
+    o = L.bbwadg_default_options()
+    o.world_size, o.rank = 2, 0
+    with pytest.raises(L.BBWADGError, match="UNSUPPORTED"):  # elastic contexts are single-GPU
+        L.bbwadg_elastic_setup(v, e, 3, 1, ones, ones, ones, o)
+    with pytest.raises(L.BBWADGError, match="UNSUPPORTED"):  # N > 9
+        L.bbwadg_elastic_setup(v, e, 10, 1, ones, ones, ones, L.bbwadg_default_options())
+    v2, e2 = tri2d.tri_mesh(2)
+    c2 = np.ones((len(e2), 3))
+    with pytest.raises(L.BBWADGError, match="MESH"):  # clockwise triangles are rejected, never reordered
+        L.bbwadg2d_setup(v2, np.ascontiguousarray(e2[:, [0, 2, 1]]), 3, 1, c2, L.bbwadg_default_options())
+    with pytest.raises(L.BBWADGError, match="NONPOSITIVE_C2"):
+        L.bbwadg2d_setup(v2, e2, 3, 1, -c2, L.bbwadg_default_options())
+    with pytest.raises(L.BBWADGError, match="UNSUPPORTED"):  # M > N
+        L.bbwadg2d_setup(v2, e2, 2, 3, np.ones((len(e2), 10)), L.bbwadg_default_options())
+    bad = np.ascontiguousarray(e2.copy())
+    bad[0, 0] = 10 ** 6
+    with pytest.raises(L.BBWADGError, match="MESH"):  # vertex id out of range
+        L.bbwadg2d_setup(v2, bad, 3, 1, c2, L.bbwadg_default_options())
+    o = L.bbwadg_default_options()
+    o.halo_transport = 2
+    with pytest.raises(L.BBWADGError, match="INVALID_ARG"):
+        L.bbwadg_setup(v, e, 3, 1, ones, o)
