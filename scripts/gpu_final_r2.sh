@@ -12,6 +12,8 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sta
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-sweep --no-config4 --elastic '' --two-d '' \
   > gpurun_out/ncu_r2_c5.log 2>&1
 ncu -i gpurun_out/prof_r2_c5.ncu-rep --page raw --csv > gpurun_out/traffic_N7M4f64.csv 2>/dev/null
+python scripts/ncu_phases.py gpurun_out/prof_r2_c5.ncu-rep paper_1808_08645_b200/native/libbbwadg.so "StageCfgILi7ELi4Ed" 4088832 \
+  > gpurun_out/phases_r2_c5.txt 2>&1
 for cfg in "4 5 3 f64" "4 5 3 f32" "3 9 9 f64"; do
   set -- $cfg
   timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
@@ -27,4 +29,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:stag
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-sweep --no-config4 --n-cubes 8 --elastic '' \
   --two-d 7:4:f64 > gpurun_out/ncu_r2_2d74.log 2>&1
 ncu -i gpurun_out/prof_r2_2d74.ncu-rep --page raw --csv > gpurun_out/t2d74_raw.csv 2>/dev/null
+mkdir -p /tmp/ncu_reps && mv gpurun_out/*.ncu-rep /tmp/ncu_reps/ 2>/dev/null  # keep gpurun_out under 64 MiB
 ls -la gpurun_out | tail -20
