@@ -207,7 +207,12 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        # the peer-read halo needs no NCCL: a gloo group carries the handle exchange and the max-over-ranks
+        # timing (so several ranks may also share one GPU, as in the 1-GPU test box)
+        if args.halo == "peer":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_1808_08645_b200 import Solver
     from paper_1808_08645_b200 import lib as L
 
@@ -216,7 +221,8 @@ def run_ours(args):
     v, e, cfunc, cuts, wname = build_workload(args, rank, world, device=dev)
     c2, c2_gids = local_c2(v, e, cfunc, M, rank, world, cuts, dev)
     nccl_id = None
-    if world > 1:
+    peer = args.halo == "peer"
+    if world > 1 and not peer:
         import torch.distributed as dist
 
         idbuf = [L.bbwadg_nccl_unique_id() if rank == 0 else None]
@@ -224,7 +230,15 @@ def run_ours(args):
         nccl_id = idbuf[0]
     stream = torch.cuda.current_stream(dev)
     s = Solver(v, e, N, M, c2, dtype=args.dtype, device=local, stream=stream, rank=rank, world_size=world,
-               nccl_id=nccl_id, partition=cuts if world > 1 else None, c2_gids=c2_gids)
+               nccl_id=nccl_id, partition=cuts if world > 1 else None, c2_gids=c2_gids,
+               halo_transport=1 if (peer and world > 1) else 0)
+    if peer and world > 1:  # peer-read halo: map every rank's state buffers and epoch flag (CUDA IPC)
+        import torch.distributed as dist
+
+        handles = [None] * world
+        dist.all_gather_object(handles, s.ipc_handles())
+        s.ipc_open_peers(handles)
+        dist.barrier()
     info = s.info()
     K_local = info["num_elements_local"]
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -261,7 +275,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device=dev if args.halo != "peer" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     K_total = info["num_elements_global"]
@@ -312,7 +326,7 @@ def run_ours(args):
         if world > 1:
             import torch.distributed as dist
 
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            t = torch.tensor([el], device=dev if args.halo != "peer" else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         sb = K_local * 4 * Np * (8 if args.dtype == "f64" else 4)
@@ -328,7 +342,9 @@ def run_ours(args):
            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
            "config": {"workload": wname, "N": N, "M": M, "K_total": K_total, "K_per_gpu": K_local,
                       "Np": Np, "dofs_per_stage": 4 * K_total * Np,
-                      "parallelism": f"element-partitioned x{world} (RCB cuts {list(cuts)}) + NCCL face-trace halo"
+                      "parallelism": f"element-partitioned x{world} (RCB cuts {list(cuts)}) + "
+                                     + ("peer-read halo (CUDA IPC, device stage barrier)" if args.halo == "peer"
+                                        else "NCCL face-trace halo")
                       if world > 1 else "single GPU",
                       "l2": "inputs (state %.1f GB/GPU) far larger than the 126 MB L2; no flush needed"
                             % (K_local * 4 * Np * (8 if args.dtype == 'f64' else 4) / 1e9)},
@@ -705,6 +721,9 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
+                    help="multi-GPU face-trace transport: pack + NCCL send/recv, or peer reads of the owners' Q_in "
+                         "over CUDA IPC (halo_transport 1)")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")

@@ -216,14 +216,17 @@ bbwadg_status bbwadg_group_step(bbwadg_ctx* ctxs, int nparts, double t, double d
 /* ---- peer-read halo across processes (halo_transport = 1, world_size > 1): CUDA IPC mapping of the
  * partitions' state buffers, so the stage kernel reads neighbour face traces from the owner's Q_in in
  * place (over NVLink between GPUs; also valid for several processes sharing one GPU).
- * bbwadg_ipc_get_handles: out[2][64] = cudaIpcMemHandle_t of this context's two state buffers.
+ * bbwadg_ipc_get_handles: out[3][64] = cudaIpcMemHandle_t of this context's two state buffers and of its
+ *                         stage-epoch flag (partitioned halo_transport 1 contexts only).
  * bbwadg_ipc_open_peer:   map the handles of rank `peer` (from its bbwadg_ipc_get_handles, exchanged by
  *                         the caller); every rank that owns a neighbour of this partition must be opened.
- * bbwadg_stage:           one LSRK45 stage s (0..4) of the state at stage time t + c_s dt.  Between two
- *                         stages every rank must have finished the previous one before any rank starts the
- *                         next (the caller's barrier + bbwadg_synchronize), because the kernel reads the
- *                         peers' stage inputs; bbwadg_step refuses IPC peer contexts for that reason.
- *                         Works for every context (s = 0..4 in order is one bbwadg_step). */
+ * Stages of IPC peers are ordered ON THE DEVICE: before stage e a one-warp kernel waits (acquire, system
+ * scope, bounded spin) until every opened peer has published epoch >= e-1, and after the stage the own epoch
+ * is published (release), so bbwadg_step / bbwadg_run need no host barrier; a peer that stops advancing
+ * makes bbwadg_run fail with BBWADG_ERR_CUDA after ~30 s instead of hanging.  All ranks must call the same
+ * sequence of stages (set_state / get_state are not synchronised: barrier around them).
+ * bbwadg_stage:           one LSRK45 stage s (0..4) of the state at stage time t + c_s dt (s = 0..4 in order
+ *                         is one bbwadg_step); works for every context. */
 bbwadg_status bbwadg_ipc_get_handles(bbwadg_ctx ctx, void* out);
 bbwadg_status bbwadg_ipc_open_peer(bbwadg_ctx ctx, int peer, const void* handles);
 bbwadg_status bbwadg_stage(bbwadg_ctx ctx, int s, double t, double dt);

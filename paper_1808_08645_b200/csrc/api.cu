@@ -89,6 +89,11 @@ struct bbwadg_ctx_s {
   int* d_gmap = nullptr;
   void* peer_q[8][2] = {};
   bool peer_ipc[8] = {};
+  // device-side stage barrier of IPC peers: own epoch flag (stages completed), the peers' mapped flags
+  unsigned long long* d_epoch = nullptr;
+  unsigned long long* peer_epoch[8] = {};
+  unsigned long long epoch = 0;
+  int* d_sync_err = nullptr;
   // multi-GPU
   nccl::Comm comm = nullptr;
   cudaStream_t comm_stream = nullptr;
@@ -300,6 +305,33 @@ bbwadg_status halo_nccl(bbwadg_ctx c, const void* Q) {
   return BBWADG_OK;
 }
 
+// Device-side barrier between LSRK stages of IPC peers (peer-read halo): before stage e every peer must have
+// completed stage e-1 (its stage output is this stage's neighbour input, and it no longer reads the buffer
+// this stage overwrites).  One thread per peer polls the peer's epoch flag (acquire, system scope) with a
+// bounded spin (timeout -> error flag, no hang); after the stage one thread publishes the own epoch (release).
+struct PeerFlags {
+  const unsigned long long* f[8];
+  int n;
+};
+__global__ void peer_wait_kernel(PeerFlags pf, unsigned long long target, int* err) {
+  const int i = threadIdx.x;
+  if (i >= pf.n) return;
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(pf.f[i]) : "memory");
+    if (v >= target) break;
+    if (clock64() - t0 > 60000000000LL) {  // ~30 s at 2 GHz
+      atomicExch(err, 1);
+      break;
+    }
+    __nanosleep(2000);
+  }
+}
+__global__ void epoch_signal_kernel(unsigned long long* flag, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
+}
+
 // One pass (stage or rhs) over all local elements including the halo exchange when partitioned.
 bbwadg_status full_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, double rk_a, double rk_b, double dt,
                         double tstage) {
@@ -313,7 +345,20 @@ bbwadg_status full_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, dou
       if (r != P.rank && P.recv_off[r + 1] > P.recv_off[r] && !c->peer_q[r][c->cur])
         return fail(c, BBWADG_ERR_INVALID_ARG, "peer-read halo: a neighbour partition's state is not mapped");
     if (Qin != c->d_Q[c->cur]) return fail(c, BBWADG_ERR_INVALID_ARG, "peer-read halo works on the context state only");
-    return launch_pass(c, mode, Qin, Qout, 0, P.K_local, rk_a, rk_b, dt, tstage);
+    PeerFlags pf{};
+    for (int r = 0; r < P.nparts && r < 8; ++r)
+      if (c->peer_epoch[r]) pf.f[pf.n++] = c->peer_epoch[r];
+    if (pf.n > 0) {
+      peer_wait_kernel<<<1, 32, 0, c->stream>>>(pf, c->epoch, c->d_sync_err);
+      CUDA_TRY(c, cudaGetLastError());
+    }
+    bbwadg_status st = launch_pass(c, mode, Qin, Qout, 0, P.K_local, rk_a, rk_b, dt, tstage);
+    if (st) return st;
+    if (c->d_epoch) {
+      epoch_signal_kernel<<<1, 1, 0, c->stream>>>(c->d_epoch, ++c->epoch);
+      CUDA_TRY(c, cudaGetLastError());
+    }
+    return BBWADG_OK;
   }
   if (P.nparts > 1 && c->comm) {
     bbwadg_status s = halo_nccl(c, Qin);
@@ -535,6 +580,10 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   }
   const int64_t nghost = P.num_ghost(), nsend = P.send_off.empty() ? 0 : P.send_off.back();
   c->transport = o.halo_transport;
+  if (c->transport == 1 && nparts > 1) {
+    CUDA_TRY(c.get(), cudaMalloc(&c->d_epoch, 256));  // own allocation: exported by CUDA IPC
+    CUDA_TRY(c.get(), cudaMemset(c->d_epoch, 0, 256));
+  }
   if (c->transport == 1 && nghost > 0) {
     CUDA_TRY(c.get(), cudaMalloc(&c->d_gmap, sizeof(int) * 2 * nghost));
     CUDA_TRY(c.get(), cudaMemcpy(c->d_gmap, P.gmap.data(), sizeof(int) * 2 * nghost, cudaMemcpyHostToDevice));
@@ -936,9 +985,11 @@ bbwadg_status bbwadg_stage(bbwadg_ctx c, int s, double t, double dt) {
 bbwadg_status bbwadg_ipc_get_handles(bbwadg_ctx c, void* out) {
   if (!c || !out) return fail(c, BBWADG_ERR_INVALID_ARG, "null argument");
   CUDA_TRY(c, cudaSetDevice(c->device));
-  for (int b = 0; b < 2; ++b) {
+  if (!c->d_epoch) return fail(c, BBWADG_ERR_INVALID_ARG, "context is not a partitioned halo_transport 1 context");
+  void* bufs[3] = {c->d_Q[0], c->d_Q[1], c->d_epoch};
+  for (int b = 0; b < 3; ++b) {
     cudaIpcMemHandle_t h;
-    CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->d_Q[b]));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&h, bufs[b]));
     std::memcpy(static_cast<char*>(out) + 64 * b, &h, 64);
   }
   return BBWADG_OK;
@@ -951,17 +1002,22 @@ bbwadg_status bbwadg_ipc_open_peer(bbwadg_ctx c, int peer, const void* handles) 
   if (peer == c->part.rank) return fail(c, BBWADG_ERR_INVALID_ARG, "a rank does not open its own handles");
   if (c->peer_ipc[peer]) return BBWADG_OK;
   CUDA_TRY(c, cudaSetDevice(c->device));
-  for (int b = 0; b < 2; ++b) {
+  void* mapped[3] = {nullptr, nullptr, nullptr};
+  for (int b = 0; b < 3; ++b) {
     cudaIpcMemHandle_t h;
     std::memcpy(&h, static_cast<const char*>(handles) + 64 * b, 64);
-    void* p = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    cudaError_t e = cudaIpcOpenMemHandle(&mapped[b], h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) {
-      if (b == 1) cudaIpcCloseMemHandle(c->peer_q[peer][0]);
-      c->peer_q[peer][0] = nullptr;
+      for (int j = 0; j < b; ++j) cudaIpcCloseMemHandle(mapped[j]);
       return fail(c, BBWADG_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
     }
-    c->peer_q[peer][b] = p;
+  }
+  c->peer_q[peer][0] = mapped[0];
+  c->peer_q[peer][1] = mapped[1];
+  c->peer_epoch[peer] = static_cast<unsigned long long*>(mapped[2]);
+  if (!c->d_sync_err) {
+    CUDA_TRY(c, cudaMalloc(&c->d_sync_err, sizeof(int)));
+    CUDA_TRY(c, cudaMemset(c->d_sync_err, 0, sizeof(int)));
   }
   c->peer_ipc[peer] = true;
   return BBWADG_OK;
@@ -970,8 +1026,6 @@ bbwadg_status bbwadg_ipc_open_peer(bbwadg_ctx c, int peer, const void* handles) 
 bbwadg_status bbwadg_step(bbwadg_ctx c, double t, double dt) {
   if (!c) return fail(c, BBWADG_ERR_INVALID_ARG, "null ctx");
   if (c->group) return fail(c, BBWADG_ERR_INVALID_ARG, "use bbwadg_group_step for group contexts");
-  if (c->transport == 1 && c->part.nparts > 1)
-    return fail(c, BBWADG_ERR_INVALID_ARG, "peer-read (IPC) contexts advance by bbwadg_stage with a barrier between stages");
   CUDA_TRY(c, cudaSetDevice(c->device));
   for (int s = 0; s < 5; ++s) {
     bbwadg_status st = full_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], RK_A[s], RK_B[s], dt, t + RK_C[s] * dt);
@@ -1063,9 +1117,11 @@ bbwadg_status bbwadg_run(bbwadg_ctx c, double t0, double dt, int64_t nsteps) {
       nonfinite_kernel<float><<<592, 256, 0, c->stream>>>(static_cast<const float*>(c->d_Q[c->cur]), n, c->d_flag);
     CUDA_TRY(c, cudaGetLastError());
   }
-  int flag = 0;
+  int flag = 0, serr = 0;
   CUDA_TRY(c, cudaMemcpyAsync(&flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (c->d_sync_err) CUDA_TRY(c, cudaMemcpyAsync(&serr, c->d_sync_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (serr) return fail(c, BBWADG_ERR_CUDA, "peer stage barrier timed out (a peer stopped advancing)");
   if (c->comm) {
     const int ne = nccl::async_error(c->comm);
     if (ne != 0 && ne != 7) {
@@ -1157,11 +1213,14 @@ void bbwadg_destroy(bbwadg_ctx c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (int r = 0; r < 8; ++r)
-    if (c->peer_ipc[r])
+    if (c->peer_ipc[r]) {
       for (int b = 0; b < 2; ++b)
         if (c->peer_q[r][b]) cudaIpcCloseMemHandle(c->peer_q[r][b]);
+      if (c->peer_epoch[r]) cudaIpcCloseMemHandle(c->peer_epoch[r]);
+    }
   void* bufs[] = {c->d_tab, c->d_Q[0], c->d_Q[1], c->d_res, c->d_c2, c->d_geo, c->d_nbr, c->d_code,
-                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag, c->d_ptime, c->d_gmap};
+                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag, c->d_ptime, c->d_gmap,
+                  c->d_epoch, c->d_sync_err};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (c->comm) nccl::comm_destroy(c->comm);

@@ -188,13 +188,13 @@ def bbwadg_stage(ctx, s: int, t: float, dt: float):
 
 
 def bbwadg_ipc_get_handles(ctx) -> bytes:
-    buf = ctypes.create_string_buffer(128)
+    buf = ctypes.create_string_buffer(192)
     _check(_L.bbwadg_ipc_get_handles(ctx, buf), ctx)
     return buf.raw
 
 
 def bbwadg_ipc_open_peer(ctx, peer: int, handles: bytes):
-    buf = ctypes.create_string_buffer(bytes(handles), 128)
+    buf = ctypes.create_string_buffer(bytes(handles), 192)
     _check(_L.bbwadg_ipc_open_peer(ctx, peer, buf), ctx)
 
 

@@ -25,7 +25,8 @@ class Solver:
 
     def __init__(self, vertices, elements, N: int, M: int, c2, *, dtype: str = "f64", tau_p: float = 1.0,
                  tau_u: float = 1.0, device: int = 0, stream=None, rank: int = 0, world_size: int = 1,
-                 nccl_id: bytes | None = None, partition=None, check_c2: bool = True, c2_gids=None):
+                 nccl_id: bytes | None = None, partition=None, check_c2: bool = True, c2_gids=None,
+                 halo_transport: int = 0):
         import torch
 
         self.torch = torch
@@ -53,7 +54,8 @@ class Solver:
         self.stream = stream
         o.rank, o.world_size = int(rank), int(world_size)
         self._nccl_id = None
-        if world_size > 1:
+        o.halo_transport = int(halo_transport)
+        if world_size > 1 and halo_transport == 0:
             if nccl_id is None:
                 raise ValueError("world_size > 1 needs the NCCL unique id (bbwadg_nccl_unique_id on rank 0)")
             import ctypes
@@ -125,6 +127,17 @@ class Solver:
 
     def step(self, t: float, dt: float):
         L.bbwadg_step(self.ctx, t, dt)
+
+    def ipc_handles(self) -> bytes:
+        """CUDA IPC handles of this partition's state buffers and stage-epoch flag (halo_transport 1)."""
+        return L.bbwadg_ipc_get_handles(self.ctx)
+
+    def ipc_open_peers(self, handles):
+        """Map every other rank's handles (list indexed by rank, e.g. from all_gather_object)."""
+        info = self.info()
+        for r, h in enumerate(handles):
+            if r != info["rank"]:
+                L.bbwadg_ipc_open_peer(self.ctx, r, h)
 
     def run(self, t0: float, dt: float, nsteps: int):
         L.bbwadg_run(self.ctx, t0, dt, nsteps)

@@ -1,12 +1,13 @@
 """Two (or more) processes, one partition each, peer-read halo over CUDA IPC (halo_transport 1).
 
     python -m torch.distributed.run --nproc-per-node P --master-addr 127.0.0.1 --master-port 29533 \
-        scripts/ipc_halo_parity.py OUT.npz [n N M steps]
+        scripts/ipc_halo_parity.py OUT.npz [n N M steps [host|device]]
 
 Each rank sets up its partition of the Kuhn mesh with world_size P, exports the CUDA IPC handles of its
-two state buffers, opens every other rank's (exchanged over a gloo process group), and advances
-`steps` LSRK45 steps by bbwadg_stage with a host barrier + stream synchronisation between stages (the
-stage kernel reads the peers' stage inputs in place).  Rank 0 gathers the final state in global order and
+two state buffers and its stage-epoch flag, opens every other rank's (exchanged over a gloo process group),
+and advances `steps` LSRK45 steps either by bbwadg_stage with a host barrier + stream synchronisation
+between stages ("host"), or by one bbwadg_run whose stages are ordered by the library's device-side epoch
+barrier alone ("device"; the stage kernel reads the peers' stage inputs in place).  Rank 0 gathers the final state in global order and
 writes OUT.npz (state, per-rank K_local / halo faces).  Works with several processes sharing one GPU
 (the test on the 1-GPU box) or one process per GPU (NVLink peer reads).
 """
@@ -27,6 +28,7 @@ from workloads import kuhn, media, states  # noqa: E402
 def main():
     out = sys.argv[1]
     n, N, M, steps = (int(x) for x in (sys.argv[2:6] if len(sys.argv) >= 6 else (4, 5, 3, 3)))
+    mode = sys.argv[6] if len(sys.argv) >= 7 else "host"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo")
     dev = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
@@ -48,11 +50,17 @@ def main():
         if r != rank:
             L.bbwadg_ipc_open_peer(ctx, r, handles[r])
     dt = 1e-3
-    for i in range(steps):
-        for s in range(5):
-            L.bbwadg_stage(ctx, s, i * dt, dt)
-            L.bbwadg_synchronize(ctx)
-            dist.barrier()
+    dist.barrier()
+    if mode == "device":
+        L.bbwadg_run(ctx, 0.0, dt, steps)  # stages ordered by the device-side epoch barrier
+    else:
+        for i in range(steps):
+            for s in range(5):
+                L.bbwadg_stage(ctx, s, i * dt, dt)
+                L.bbwadg_synchronize(ctx)
+                dist.barrier()
+    L.bbwadg_synchronize(ctx)
+    dist.barrier()
     loc = np.empty((len(gid), 4, states.num_coeffs(N)))
     L.bbwadg_get_state(ctx, loc, 0)
     parts = [None] * world

@@ -312,19 +312,21 @@ def test_group_peer_read_halo_is_bitwise(gpu_lib, nparts, N, M):
     assert np.array_equal(out, ref)
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_ipc_peer_read_halo_across_processes(gpu_lib, tmp_path, world):
+@pytest.mark.parametrize("world,mode", [(2, "host"), (3, "host"), (2, "device"), (3, "device")])
+def test_ipc_peer_read_halo_across_processes(gpu_lib, tmp_path, world, mode):
     """`world` processes (sharing the one GPU of the test box), one partition each, CUDA-IPC-mapped state
-    buffers, bbwadg_stage + barrier: the gathered state equals the single-process run bitwise."""
+    buffers; stages ordered by bbwadg_stage + host barrier, or by bbwadg_run alone (device-side epoch barrier
+    over the mapped flags): the gathered state equals the single-process run bitwise."""
     import subprocess
     import sys
 
     N, M, n, steps = 5, 3, 4, 3
     outf = tmp_path / "ipc.npz"
-    port = 29533 + world
+    port = 29533 + world + (10 if mode == "device" else 0)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(world),
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "scripts/ipc_halo_parity.py",
-                        str(outf), str(n), str(N), str(M), str(steps)], capture_output=True, text=True, timeout=600)
+                        str(outf), str(n), str(N), str(M), str(steps), mode], capture_output=True, text=True,
+                       timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     d = np.load(outf)
     assert np.all(d["halo"] > 0)
