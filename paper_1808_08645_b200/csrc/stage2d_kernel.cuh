@@ -9,7 +9,9 @@
 //   LSRK     res = a_s res + dt rhs; Q_out = Q_in + b_s res
 // Factorial-scaled unweighted sums as in 3D (layout.hpp).  Groups of TG lanes per element (sub-warp for
 // N <= 4), CTAs of 128 threads, a persistent grid-stride loop; shared memory per element holds the stencil
-// arrays, the WADG work region aliases the volume / surface region.
+// arrays, the WADG work region aliases the volume / surface region.  The LSRK state is read at the output
+// (measured: holding it in registers from the element start costs 7-14 % at (7,4), (3,1), (9,2) in fp64 --
+// 8 more registers, one CTA per SM less -- and gains 4 % in fp32 only).
 #pragma once
 #include "layout2d.hpp"
 #include "stage_kernel.cuh"
@@ -87,17 +89,6 @@ __global__ void __launch_bounds__(C::T) stage2d_kernel(const Stage2DArgs<R> A) {
     const long long k = A.elem_begin + batch;
     const bool live = batch < nelem;
     R ru[2][KO];
-    // LSRK state of the lane's coefficients: the residual is requested now (its HBM latency hides behind the
-    // whole stage), the own Q_in is copied from shared memory after the loads
-    R rs[3][KO], qo[3][KO];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int kk = 0; kk < KO; ++kk) {
-        const int a = q + TG * kk;
-        rs[c][kk] = (A.mode == 0 && live && a < NP) ? __ldcs(A.res + k * 3 * NP + c * NP + a) : R(0);
-        qo[c][kk] = R(0);
-      }
     // ---- A: loads
     if (live) {
       if (A.mode == 2) {
@@ -123,10 +114,6 @@ __global__ void __launch_bounds__(C::T) stage2d_kernel(const Stage2DArgs<R> A) {
       }
       if (q < 3) ST(C::X_G + q * (NPM1 + 1), R(0));  // zero slots of G''
       if (q < 6) ST(C::X_Y + q * NE, R(0));          // zero slots of Y''
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int kk = 0; kk < KO; ++kk) qo[c][kk] = LD(C::X_Q + c * NP + cmin(q + TG * kk, NP - 1));
       sync();
       const int* nbs = reinterpret_cast<const int*>(gb + 16 * RB);
       const uint8_t* cds = reinterpret_cast<const uint8_t*>(gb + 16 * RB + 12);
@@ -275,9 +262,9 @@ __global__ void __launch_bounds__(C::T) stage2d_kernel(const Stage2DArgs<R> A) {
               for (int d = 0; d < 2; ++d) {
                 const long long gi = k * 3 * NP + (1 + d) * NP + a;
                 if (A.mode == 0) {
-                  const R r = fma(A.rk_a, rs[1 + d][kk], A.dt * r2[d]);
+                  const R r = fma(A.rk_a, __ldcs(A.res + gi), A.dt * r2[d]);
                   A.res[gi] = r;
-                  A.Qout[gi] = fma(A.rk_b, r, qo[1 + d][kk]);
+                  A.Qout[gi] = fma(A.rk_b, r, __ldg(A.Qin + gi));
                 } else {
                   A.Qout[gi] = r2[d];
                 }
@@ -374,9 +361,9 @@ __global__ void __launch_bounds__(C::T) stage2d_kernel(const Stage2DArgs<R> A) {
       } else {
         const long long gi = k * 3 * NP + a;
         if (A.mode == 0) {
-          const R r = fma(A.rk_a, rs[0][kk], A.dt * dp[kk]);
+          const R r = fma(A.rk_a, __ldcs(A.res + gi), A.dt * dp[kk]);
           A.res[gi] = r;
-          A.Qout[gi] = fma(A.rk_b, r, qo[0][kk]);
+          A.Qout[gi] = fma(A.rk_b, r, __ldg(A.Qin + gi));
         } else {
           A.Qout[gi] = dp[kk];
         }
