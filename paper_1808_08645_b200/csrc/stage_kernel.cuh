@@ -265,6 +265,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 #ifndef BBW_TMA
 #define BBW_TMA 1  // element Q blocks, geometry and neighbour ids by cp.async.bulk (needs BBW_CPASYNC)
 #endif
+#ifndef BBW_FLUX_LATE
+#define BBW_FLUX_LATE 0  // fluxes (B1b) after C1: measured -6 % at (7,4) and -5 % at (5,3) (register spills; rejected)
+#endif
 #ifndef BBW_TMA_MIN_TG
 #define BBW_TMA_MIN_TG 32  // TMA only for whole-warp groups (sub-warp groups: cp.async; see the kernel)
 #endif
@@ -1338,6 +1341,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
           }
         }
       }
+      auto flux_phase = [&]() {
       // ---- B1b: fluxes, F' = |grad l_f| c! F  (boundary: p+ = -p, u+ = u, R11)
 #pragma unroll
       for (int k = 0; k < K1; ++k) {
@@ -1367,6 +1371,10 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
           }
         }
       }
+      };
+#if !BBW_FLUX_LATE
+      flux_phase();
+#endif
 #if BBW_LSRK_REG
       // ---- B0: own Q -> registers (LSRK)
 #pragma unroll
@@ -1422,6 +1430,11 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
           }
         }
       }
+#if BBW_FLUX_LATE
+      // the fluxes after the volume elevation: the neighbour-trace loads of B1a have B2 and C1 to arrive
+      flux_phase();
+      sync();
+#endif
       // ---- C2: Y''[ff][d] = (sum_s F'[ff][d + e_s]) / (d!)^2
       face_sum3<C, R, NFP1, C::Y_F, NFP, C::Y_Y + 1, NFP1 + 1, true>(
           gb, q, reinterpret_cast<const ushort4*>(tab + L.trired) + trired_off(N - 1),
