@@ -176,3 +176,49 @@ def test_2d_setup_validates(gpu_lib, mesh6):
         _solver(v, e, 3, 1, -c2)
     with pytest.raises(ValueError):
         _solver(v, e, 3, 1, c2[:, :2])
+
+
+def _closure2(e, sample):
+    """sample triangles plus every triangle sharing an edge with one of them."""
+    K = e.shape[0]
+    edges = np.concatenate([np.sort(e[:, [1, 2]], 1), np.sort(e[:, [0, 2]], 1), np.sort(e[:, [0, 1]], 1)])
+    owner = np.concatenate([np.arange(K)] * 3)
+    order = np.lexsort((edges[:, 1], edges[:, 0]))
+    se, so = edges[order], owner[order]
+    same = np.all(se[1:] == se[:-1], axis=1)
+    a, b = so[:-1][same], so[1:][same]
+    want = np.zeros(K, dtype=bool)
+    want[sample] = True
+    return np.unique(np.concatenate([sample, b[want[a]], a[want[b]]]))
+
+
+@pytest.mark.parametrize("N,M,dtype,tol", [(7, 4, "f64", 1e-12), (7, 4, "f32", 1e-5), (9, 2, "f64", 1e-12),
+                                           (3, 1, "f64", 1e-12)])
+def test_2d_full_size_sampled_parity(gpu_lib, N, M, dtype, tol):
+    """bench.py's 2D workload at full size (n = 512, 524,288 triangles, smooth c^2) in the bench launch
+    configuration: one bbwadg_rhs; the oracle recomputes 48 sampled triangles (with their edge neighbours)."""
+    import torch
+
+    n = 512
+    v, e = tri2d.tri_mesh(n)
+    c2 = tri2d.project_c2(v, e, tri2d.c2_smooth_2d(1.0), M)
+    dev = torch.device("cuda", 0)
+    s = _solver(v, e, N, M, c2, dtype=dtype)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(2808)
+    Q = torch.randn((len(e), 3, tri2d.num_coeffs(N)), dtype=torch.float64, device=dev, generator=gen)
+    if dtype == "f32":
+        Q = Q.float()
+    out = s.rhs(Q, 0.0)
+    rng = np.random.default_rng(7)
+    sample = np.unique(np.concatenate([rng.choice(len(e), 46, replace=False), [0, len(e) - 1]]))
+    sub = _closure2(e, sample)
+    idx = torch.from_numpy(sub).to(dev)
+    Qs = Q.index_select(0, idx).double().cpu().numpy()
+    got = out.index_select(0, idx).double().cpu().numpy()
+    del out, Q
+    s.close()
+    ref = Acoustic2DOracle(v, e[sub], N, M, c2[sub]).rhs(Qs)
+    pos = np.searchsorted(sub, sample)
+    assert rel_l2(got[pos], ref[pos]) <= tol
+    assert field_max_rel(got[pos], ref[pos]) <= 10 * tol

@@ -202,3 +202,51 @@ def test_elastic_setup_validates(gpu_lib, mesh3):
     with pytest.raises(L.BBWADGError):
         s.set_source(np.zeros((K, ew.num_coeffs(3))))
     assert s.info()["Np"] == 20 and mp == 4
+
+
+def _closure3(e, sample):
+    """sample tets plus every tet sharing a face with one of them."""
+    K = e.shape[0]
+    faces = np.concatenate([np.sort(e[:, [1, 2, 3]], 1), np.sort(e[:, [0, 2, 3]], 1),
+                            np.sort(e[:, [0, 1, 3]], 1), np.sort(e[:, [0, 1, 2]], 1)])
+    owner = np.concatenate([np.arange(K)] * 4)
+    order = np.lexsort((faces[:, 2], faces[:, 1], faces[:, 0]))
+    sf, so = faces[order], owner[order]
+    same = np.all(sf[1:] == sf[:-1], axis=1)
+    a, b = so[:-1][same], so[1:][same]
+    want = np.zeros(K, dtype=bool)
+    want[sample] = True
+    return np.unique(np.concatenate([sample, b[want[a]], a[want[b]]]))
+
+
+@pytest.mark.parametrize("N,M,dtype,tol", [(7, 2, "f64", 1e-12), (7, 2, "f32", 1e-5), (9, 2, "f64", 1e-12)])
+def test_elastic_full_size_sampled_parity(gpu_lib, N, M, dtype, tol):
+    """bench.py's elastic workload at full size (n = 56, 1,053,696 tets, smooth Lame fields) in the bench
+    launch configuration: one bbwadg_rhs over the whole mesh; the oracle recomputes 48 sampled tets (with
+    their face neighbours), per field / element maxima beside the pooled error."""
+    import torch
+
+    n = 56
+    v, e = kuhn.kuhn_mesh(n)
+    dev = torch.device("cuda", 0)
+    mats = ew.smooth_material(v, e, M, device=dev)
+    s = _solver(v, e, N, M, mats, dtype=dtype)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1809)
+    Q = torch.randn((len(e), 9, ew.num_coeffs(N)), dtype=torch.float64, device=dev, generator=gen)
+    if dtype == "f32":
+        Q = Q.float()
+    out = s.rhs(Q, 0.0)
+    rng = np.random.default_rng(6)
+    sample = np.unique(np.concatenate([rng.choice(len(e), 46, replace=False), [0, len(e) - 1]]))
+    sub = _closure3(e, sample)
+    idx = torch.from_numpy(sub).to(dev)
+    Qs = Q.index_select(0, idx).double().cpu().numpy()
+    got = out.index_select(0, idx).double().cpu().numpy()
+    del out, Q
+    s.close()
+    o = ElasticOracle(v, e[sub], N, M, *(m[sub] for m in mats))
+    ref = o.rhs(Qs)
+    pos = np.searchsorted(sub, sample)
+    assert rel_l2(got[pos], ref[pos]) <= tol
+    assert field_max_rel(got[pos], ref[pos]) <= 10 * tol
