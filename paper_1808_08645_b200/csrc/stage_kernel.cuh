@@ -106,7 +106,9 @@ struct StageCfg {
 #ifdef BBW_MINB
   static constexpr int MINB = BBW_MINB;
 #else
-  static constexpr int MINB = default_minb(N);
+  // fp32 (half the element block): 6 CTAs per SM for the whole-warp groups of N = 5..7 (A/B: +9.3 % at (7,4),
+  // +1.9 % at (5,3); 8 CTAs spills and is slower), the fp64 choice elsewhere
+  static constexpr int MINB = (sizeof(R) == 4 && N >= 5 && N <= 7) ? 6 : default_minb(N);
 #endif
   static constexpr int G = T / TG;               // groups per CTA
   static constexpr int KO = (NP + TG - 1) / TG;  // owned coefficients per thread

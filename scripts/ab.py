@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """A/B tuning variants of libbbwadg.so (library vs library; no oracle).
 
-    python scripts/ab.py N M ref_variant var1 [var2 ...]
+    [AB_DTYPE=f32] [AB_NCUBE=n] python scripts/ab.py N M ref_variant var1 [var2 ...]
 
 For every variant (a directory under paper_1808_08645_b200/native/, or `default`), a
 subprocess computes one RHS and 3 LSRK steps on a random state of an n=6 Kuhn mesh and
@@ -21,16 +21,18 @@ from workloads.media import random_c2
 from workloads.states import random_state
 from paper_1808_08645_b200.solver import Solver
 N, M, tag, ncube = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], int(sys.argv[4])
+import os
+dt = os.environ.get("AB_DTYPE", "f64")
 v, e = kuhn_mesh(6)
-s = Solver(v, e, N, M, random_c2(len(e), M))
-Q = torch.tensor(random_state(len(e), N), device="cuda")
+s = Solver(v, e, N, M, random_c2(len(e), M), dtype=dt)
+Q = torch.tensor(random_state(len(e), N), device="cuda", dtype=torch.float64 if dt == "f64" else torch.float32)
 r = s.rhs(Q).cpu().numpy()
 s.set_state(random_state(len(e), N)); s.run(0.0, 1e-3, 3); q3 = s.get_state()
 np.save(f"/tmp/ab_{tag}_rhs.npy", r); np.save(f"/tmp/ab_{tag}_q3.npy", np.asarray(q3))
 s.close()
 v, e = kuhn_mesh(ncube)
 from workloads.media import project_c2, c2_smooth
-s = Solver(v, e, N, M, random_c2(len(e), M, lo=0.9, hi=1.1))
+s = Solver(v, e, N, M, random_c2(len(e), M, lo=0.9, hi=1.1), dtype=dt)
 s.set_state(np.zeros((len(e), 4, (N+1)*(N+2)*(N+3)//6)))
 s.run(0.0, 1e-4, 2); s.synchronize()
 st = torch.cuda.Event(enable_timing=True); en = torch.cuda.Event(enable_timing=True)
