@@ -207,12 +207,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        # the peer-read halo needs no NCCL: a gloo group carries the handle exchange and the max-over-ranks
-        # timing (so several ranks may also share one GPU, as in the 1-GPU test box)
-        if args.halo == "peer":
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
+        # control plane over gloo (handle / NCCL-id exchange, max-over-ranks timing): the library's own
+        # transports (peer reads over CUDA IPC, or its NCCL communicator) carry the face traces
+        dist.init_process_group("gloo")
     from paper_1808_08645_b200 import Solver
     from paper_1808_08645_b200 import lib as L
 
@@ -220,25 +217,48 @@ def run_ours(args):
     Np = comb(N + 3, 3)
     v, e, cfunc, cuts, wname = build_workload(args, rank, world, device=dev)
     c2, c2_gids = local_c2(v, e, cfunc, M, rank, world, cuts, dev)
-    nccl_id = None
-    peer = args.halo == "peer"
-    if world > 1 and not peer:
-        import torch.distributed as dist
-
-        idbuf = [L.bbwadg_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idbuf, src=0)
-        nccl_id = idbuf[0]
     stream = torch.cuda.current_stream(dev)
-    s = Solver(v, e, N, M, c2, dtype=args.dtype, device=local, stream=stream, rank=rank, world_size=world,
-               nccl_id=nccl_id, partition=cuts if world > 1 else None, c2_gids=c2_gids,
-               halo_transport=1 if (peer and world > 1) else 0)
-    if peer and world > 1:  # peer-read halo: map every rank's state buffers and epoch flag (CUDA IPC)
+
+    def make_solver(transport):
+        nccl_id = None
+        if world > 1 and transport == "nccl":
+            import torch.distributed as dist
+
+            idbuf = [L.bbwadg_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idbuf, src=0)
+            nccl_id = idbuf[0]
+        return Solver(v, e, N, M, c2, dtype=args.dtype, device=local, stream=stream, rank=rank, world_size=world,
+                      nccl_id=nccl_id, partition=cuts if world > 1 else None, c2_gids=c2_gids,
+                      halo_transport=1 if (transport == "peer" and world > 1) else 0)
+
+    halo = args.halo if world > 1 else "none"
+    if halo in ("peer", "auto"):
+        # peer-read halo: map every rank's state buffers and epoch flag (CUDA IPC); "auto" falls back to the
+        # NCCL transport if any rank cannot map its peers
         import torch.distributed as dist
 
-        handles = [None] * world
-        dist.all_gather_object(handles, s.ipc_handles())
-        s.ipc_open_peers(handles)
+        s = make_solver("peer")
+        ok = 1
+        try:
+            handles = [None] * world
+            dist.all_gather_object(handles, s.ipc_handles())
+            s.ipc_open_peers(handles)
+        except Exception as ex:  # noqa: BLE001
+            if halo == "peer":
+                raise
+            print(f"rank {rank}: peer-read halo unavailable ({ex}); falling back to NCCL", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            halo = "peer"
+        else:
+            s.close()
+            halo = "nccl"
+            s = make_solver("nccl")
         dist.barrier()
+    else:
+        s = make_solver(halo)
     info = s.info()
     K_local = info["num_elements_local"]
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -247,6 +267,11 @@ def run_ours(args):
     Q0 = torch.randn((K_local, 4, Np), dtype=tdt, device=dev, generator=gen)
     s.set_state(Q0)
     del Q0
+    torch.cuda.synchronize()
+    if world > 1:  # every rank's state is in place before any stage reads a peer's (peer-read halo)
+        import torch.distributed as dist
+
+        dist.barrier()
     h_min = 2.0 / args.n_cubes / (1 + np.sqrt(2) + np.sqrt(3))  # Kuhn tet inradius-scale height bound
     dt = 0.5 * h_min / (np.sqrt(1.5) * (N + 1) ** 2)
 
@@ -275,7 +300,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], device=dev if args.halo != "peer" else "cpu", dtype=torch.float64)
+        t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     K_total = info["num_elements_global"]
@@ -317,6 +342,10 @@ def run_ours(args):
         barrier()
         t0 = time.perf_counter()
         L.bbwadg_set_state(s.ctx, hQ, 0)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
         for i in range(args.steps):
             L.bbwadg_run(s.ctx, i * dt, dt, 1)
         L.bbwadg_get_state(s.ctx, hQ, 0)
@@ -326,7 +355,7 @@ def run_ours(args):
         if world > 1:
             import torch.distributed as dist
 
-            t = torch.tensor([el], device=dev if args.halo != "peer" else "cpu", dtype=torch.float64)
+            t = torch.tensor([el], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         sb = K_local * 4 * Np * (8 if args.dtype == "f64" else 4)
@@ -343,7 +372,7 @@ def run_ours(args):
            "config": {"workload": wname, "N": N, "M": M, "K_total": K_total, "K_per_gpu": K_local,
                       "Np": Np, "dofs_per_stage": 4 * K_total * Np,
                       "parallelism": f"element-partitioned x{world} (RCB cuts {list(cuts)}) + "
-                                     + ("peer-read halo (CUDA IPC, device stage barrier)" if args.halo == "peer"
+                                     + ("peer-read halo (CUDA IPC, device stage barrier)" if halo == "peer"
                                         else "NCCL face-trace halo")
                       if world > 1 else "single GPU",
                       "l2": "inputs (state %.1f GB/GPU) far larger than the 126 MB L2; no flush needed"
@@ -721,9 +750,10 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
-                    help="multi-GPU face-trace transport: pack + NCCL send/recv, or peer reads of the owners' Q_in "
-                         "over CUDA IPC (halo_transport 1)")
+    ap.add_argument("--halo", choices=["auto", "nccl", "peer"], default="auto",
+                    help="multi-GPU face-trace transport: peer reads of the owners' Q_in over CUDA IPC (halo_transport "
+                         "1; exercised on hardware across processes), pack + NCCL send/recv, or auto = peer with a "
+                         "fallback to NCCL when the peers cannot be mapped")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
