@@ -100,6 +100,11 @@ struct bbwadg_ctx_s {
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   Group* group = nullptr;
   int group_index = 0;
+  // CUDA graphs of one LSRK step (5 stage launches), one per starting state buffer, replayed by bbwadg_run
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev = nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  double gdt = 0;
   // bookkeeping
   int64_t steps = 0;
   double t = 0;
@@ -1102,11 +1107,77 @@ bbwadg_status bbwadg_group_step(bbwadg_ctx* ctxs, int n, double t, double dt) {
   return BBWADG_OK;
 }
 
+namespace {
+// One LSRK step as a CUDA graph (the 5 stage launches captured on a private stream), for runs without a
+// time-dependent source on single-partition contexts: replaying it removes the per-launch host overhead that
+// dominates small meshes (DESIGN.md §6 "CUDA graph").  Two graphs, one per starting state buffer (a step
+// flips the ping-pong buffers an odd number of times); rebuilt when dt changes.
+bbwadg_status graph_run(bbwadg_ctx c, double t0, double dt, int64_t nsteps) {
+  if (!c->gstream) {
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->gev, cudaEventDisableTiming));
+  }
+  if (!c->gexec[0] || c->gdt != dt) {
+    for (int b = 0; b < 2; ++b)
+      if (c->gexec[b]) {
+        cudaGraphExecDestroy(c->gexec[b]);
+        c->gexec[b] = nullptr;
+      }
+    const int cur0 = c->cur;
+    cudaStream_t user = c->stream;
+    c->stream = c->gstream;  // launch_pass launches on c->stream
+    for (int b = 0; b < 2; ++b) {
+      c->cur = b;
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeThreadLocal);
+      bbwadg_status st = BBWADG_OK;
+      for (int s = 0; e == cudaSuccess && st == BBWADG_OK && s < 5; ++s) {
+        st = launch_pass(c, 0, c->d_Q[c->cur], c->d_Q[1 - c->cur], 0, c->part.K_local, RK_A[s], RK_B[s], dt,
+                         RK_C[s] * dt);
+        c->cur ^= 1;
+      }
+      cudaError_t e2 = cudaStreamEndCapture(c->gstream, &g);
+      if (e == cudaSuccess) e = e2;
+      if (e == cudaSuccess && st == BBWADG_OK) e = cudaGraphInstantiate(&c->gexec[b], g, 0);
+      if (g) cudaGraphDestroy(g);
+      if (st != BBWADG_OK || e != cudaSuccess) {
+        c->stream = user;
+        c->cur = cur0;
+        if (st != BBWADG_OK) return st;
+        return fail(c, BBWADG_ERR_CUDA, std::string("step graph: ") + cudaGetErrorString(e));
+      }
+    }
+    c->stream = user;
+    c->cur = cur0;
+    c->gdt = dt;
+  }
+  CUDA_TRY(c, cudaEventRecord(c->gev, c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->gstream, c->gev, 0));
+  for (int64_t i = 0; i < nsteps; ++i) {
+    CUDA_TRY(c, cudaGraphLaunch(c->gexec[c->cur], c->gstream));
+    c->cur ^= 1;  // 5 stages = an odd number of buffer flips
+  }
+  CUDA_TRY(c, cudaEventRecord(c->gev, c->gstream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->gev, 0));
+  c->steps += nsteps;
+  c->t = t0 + nsteps * dt;
+  return BBWADG_OK;
+}
+}  // namespace
+
 bbwadg_status bbwadg_run(bbwadg_ctx c, double t0, double dt, int64_t nsteps) {
   if (!c || nsteps < 0) return fail(c, BBWADG_ERR_INVALID_ARG, "bad arguments");
-  for (int64_t i = 0; i < nsteps; ++i) {
-    bbwadg_status s = bbwadg_step(c, t0 + i * dt, dt);
+  if (c->group) return fail(c, BBWADG_ERR_INVALID_ARG, "use bbwadg_group_step for group contexts");
+  const bool graphable = nsteps >= 2 && c->part.nparts == 1 && !c->d_src && !getenv("BBWADG_NO_GRAPH");
+  if (graphable) {
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    bbwadg_status s = graph_run(c, t0, dt, nsteps);
     if (s) return s;
+  } else {
+    for (int64_t i = 0; i < nsteps; ++i) {
+      bbwadg_status s = bbwadg_step(c, t0 + i * dt, dt);
+      if (s) return s;
+    }
   }
   CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
   long long n = (long long)c->part.K_local * c->nfields * c->Np;
@@ -1223,6 +1294,10 @@ void bbwadg_destroy(bbwadg_ctx c) {
                   c->d_epoch, c->d_sync_err};
   for (void* p : bufs)
     if (p) cudaFree(p);
+  for (int b = 0; b < 2; ++b)
+    if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
+  if (c->gev) cudaEventDestroy(c->gev);
+  if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->comm) nccl::comm_destroy(c->comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
