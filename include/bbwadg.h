@@ -158,7 +158,10 @@ bbwadg_status bbwadg_wadg_apply(bbwadg_ctx ctx, const void* r_dev, void* out_dev
 bbwadg_status bbwadg_step(bbwadg_ctx ctx, double t, double dt);
 
 /* nsteps steps from t0; synchronises at the end and checks the state for
- * NaN/Inf (BBWADG_ERR_NONFINITE). */
+ * NaN/Inf (BBWADG_ERR_NONFINITE).  On single-partition contexts without a source
+ * and nsteps >= 2 the step is replayed as a CUDA graph (5 stage launches captured
+ * once per dt on a private stream ordered with the context's stream; bitwise equal
+ * to bbwadg_step; environment variable BBWADG_NO_GRAPH disables it). */
 bbwadg_status bbwadg_run(bbwadg_ctx ctx, double t0, double dt, int64_t nsteps);
 
 /* Block until all work queued on the ctx's stream has finished. */
