@@ -82,6 +82,7 @@ struct bbwadg_ctx_s {
   void* d_send = nullptr;
   int* d_sendfaces = nullptr;
   int* d_flag = nullptr;
+  unsigned int* d_qctr = nullptr;  // stage-kernel work queue: [0] next batch ticket, [1] finished units
   unsigned long long* d_ptime = nullptr;  // phase timing counters (BBW_PHASE_TIMING builds)
   // peer-read halo (halo_transport 1): owner-rank / owner-local id per ghost slot, and the peers' two
   // state buffers (same-process group members, or CUDA-IPC mappings of other processes)
@@ -143,6 +144,7 @@ void fill_args(bbwadg_ctx c, StageArgs<R>& a) {
   a.ghost = static_cast<const R*>(c->d_ghost);
   a.src = static_cast<const R*>(c->d_src);
   a.tab = static_cast<const uint8_t*>(c->d_tab);
+  a.qctr = c->d_qctr;
   if (c->transport == 1 && c->d_gmap) {
     a.gmap = c->d_gmap;
     for (int r = 0; r < 8; ++r) a.peer[r] = static_cast<const R*>(c->peer_q[r][c->cur]);
@@ -234,6 +236,10 @@ bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, i
   if (c->dim == 2) return launch_2d_pass(c, mode, Qin, Qout, b, e, rk_a, rk_b, dt, tstage);
   int64_t nb = (e - b + c->ks.elems_per_cta - 1) / c->ks.elems_per_cta;
   int grid = (int)std::min<int64_t>(nb, grid_cap > 0 ? grid_cap : c->grid);
+  // work-queue ticket size: one unit-batch when every CTA slot runs >= 1000 batches (SM drift would otherwise
+  // spread the in-flight window; config 5: +1.7 % over 2), two below (amortises the atomic; +3.8 % at (5,3) on
+  // 1.57M elements).  A/B: profiles/r2s3_workqueue_ab.txt
+  const int qch = nb >= 1000 * (int64_t)grid ? 1 : 2;
   cudaError_t err;
   if (c->dtype == BBWADG_F64) {
     StageArgs<double> a;
@@ -249,6 +255,7 @@ bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, i
     a.src_amp = std::sin(M_PI * tstage);
     a.mode = mode;
     a.ptime = c->d_ptime;
+    a.qch = qch;
     err = c->ks.launch_stage(&a, grid, c->stream);
   } else {
     StageArgs<float> a;
@@ -264,6 +271,7 @@ bbwadg_status launch_pass(bbwadg_ctx c, int mode, const void* Qin, void* Qout, i
     a.src_amp = (float)std::sin(M_PI * tstage);
     a.mode = mode;
     a.ptime = c->d_ptime;
+    a.qch = qch;
     err = c->ks.launch_stage(&a, grid, c->stream);
   }
   if (err != cudaSuccess) return fail(c, BBWADG_ERR_CUDA, std::string("stage kernel launch: ") + cudaGetErrorString(err));
@@ -579,6 +587,8 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
   CUDA_TRY(c.get(), cudaMalloc(&c->d_res, std::max<size_t>(sb, 16)));
   CUDA_TRY(c.get(), cudaMemset(c->d_res, 0, sb));
   CUDA_TRY(c.get(), cudaMalloc(&c->d_flag, sizeof(int)));
+  CUDA_TRY(c.get(), cudaMalloc(&c->d_qctr, 2 * sizeof(unsigned int)));  // zero between launches (self-reset)
+  CUDA_TRY(c.get(), cudaMemset(c->d_qctr, 0, 2 * sizeof(unsigned int)));
   if (getenv("BBWADG_PHASE_TIMING")) {
     CUDA_TRY(c.get(), cudaMalloc(&c->d_ptime, 32 * sizeof(unsigned long long)));
     CUDA_TRY(c.get(), cudaMemset(c->d_ptime, 0, 32 * sizeof(unsigned long long)));
@@ -1290,7 +1300,7 @@ void bbwadg_destroy(bbwadg_ctx c) {
       if (c->peer_epoch[r]) cudaIpcCloseMemHandle(c->peer_epoch[r]);
     }
   void* bufs[] = {c->d_tab, c->d_Q[0], c->d_Q[1], c->d_res, c->d_c2, c->d_geo, c->d_nbr, c->d_code,
-                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag, c->d_ptime, c->d_gmap,
+                  c->d_src, c->d_ghost, c->d_send, c->d_sendfaces, c->d_flag, c->d_qctr, c->d_ptime, c->d_gmap,
                   c->d_epoch, c->d_sync_err};
   for (void* p : bufs)
     if (p) cudaFree(p);

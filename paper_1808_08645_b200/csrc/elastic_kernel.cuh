@@ -94,7 +94,25 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
 
   const long long nelem = A.elem_end - A.elem_begin;
   const int gw = grp % EC::GPW;
+#if BBW_DYNQ
+  // dynamic work queue (as stage_kernel): tickets from a global atomic keep the in-flight window a contiguous
+  // Morton range, so neighbour traces hit L2; the last unit resets the counters for the next launch
+  auto next_batch = [&]() -> long long {
+    if constexpr (TG <= 32) {
+      unsigned v = 0;
+      if ((tid & 31) == 0) v = atomicAdd(A.qctr, 1u);
+      return (long long)__shfl_sync(0xffffffffu, v, 0) * EC::GPW;
+    } else {
+      unsigned* tslot = reinterpret_cast<unsigned*>(smem_raw + EC::G * EC::GB) + 2 * grp;
+      if (q == 0) *tslot = atomicAdd(A.qctr, 1u);
+      sync();
+      return (long long)*tslot;
+    }
+  };
+  for (long long bw = next_batch(); bw < nelem; bw = next_batch()) {
+#else
   for (long long bw = (long long)blockIdx.x * EC::G + (grp - gw); bw < nelem; bw += (long long)gridDim.x * EC::G) {
+#endif
     const long long batch = bw + gw;
     const long long k = A.elem_begin + batch;
     const bool live = batch < nelem;  // sub-warp groups: idle groups run the phases on stale data, write nothing
@@ -422,6 +440,20 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
     }
     sync();
   }
+#if BBW_DYNQ
+  {
+    const bool leader = (TG <= 32) ? ((tid & 31) == 0) : (q == 0);
+    if (leader) {
+      const unsigned units = gridDim.x * (TG <= 32 ? EC::T / 32 : EC::G);
+      __threadfence();
+      if (atomicAdd(A.qctr + 1, 1u) == units - 1) {
+        A.qctr[0] = 0;
+        A.qctr[1] = 0;
+        __threadfence();
+      }
+    }
+  }
+#endif
 }
 
 }  // namespace bbw

@@ -60,6 +60,8 @@ struct StageArgs {
   const int* gmap;
   const R* src;        // [K][NP] or null
   const uint8_t* tab;  // table blob (layout.hpp)
+  unsigned int* qctr;  // BBW_DYNQ work queue [2] (zero at launch; the kernel's last unit resets it)
+  int qch;             // unit-batches per work-queue ticket (>= 1; the host picks it from the batches per unit)
   long long elem_begin, elem_end;
   R rk_a, rk_b, dt, src_amp, tau_p, tau_u;
   R gam[10], lam[10];
@@ -80,6 +82,13 @@ __host__ __device__ constexpr int default_et(int N) { return N > 0 ? 1 : 1; }
 // minimum resident CTAs per SM for __launch_bounds__ (caps registers at 65536 / (T * MINB)); A/B-measured
 // (scripts/ab_minb.sh): 5 for N = 4, 5 (+3.6 %, +2..3 %), 4 elsewhere (N=6: -5.7 %, N=7: -15 % at 5)
 __host__ __device__ constexpr int default_minb(int N) { return (N == 4 || N == 5) ? 5 : 4; }
+
+#ifndef BBW_ROWD
+#define BBW_ROWD 0  // row-owned lift layers (phase D): measured -13 % at (7,4), -19 % at (5,3), -42 % at (9,9) (spills)
+#endif
+#ifndef BBW_FPAD
+#define BBW_FPAD 2  // face-array padding (reals) for the row-owned layer sweep
+#endif
 
 #ifndef BBW_TRIPLE
 #define BBW_TRIPLE 2  // shell-order ownership of the WADG projection: 1 always, 0 never, 2 where it measured faster
@@ -116,7 +125,11 @@ struct StageCfg {
   static constexpr int O_GEO = 0, O_C = 40, O_RP = 40 + MP;  // GEO: grad l (12), normals+|grad l| (16), nbr/code ints
   static constexpr int O_X = rup(O_RP + NP, VEC);
   static constexpr int X_Q = O_X, X_G = O_X + 4 * NP, X_L = O_X;  // Q + G'', later the lift layers
-  static constexpr int XSIZE = cmax(4 * NP + 4 * (NPM1 + 1), 8 * NP);
+  // lift-layer arrays: 8 face/flux arrays of NP reals (layers j = 0..N concatenated) at stride FS; the
+  // row-owned layer sweep (BBW_ROWD) pads FS so the 8 arrays start in different shared-memory banks
+  static constexpr bool ROWD = BBW_ROWD && TG >= 32 && ET == 1;
+  static constexpr int FS = ROWD ? NP + BBW_FPAD : NP;
+  static constexpr int XSIZE = cmax(4 * NP + 4 * (NPM1 + 1), 8 * FS);
   static constexpr int O_Y = O_X + XSIZE;
   static constexpr int Y_F = O_Y, Y_Y = O_Y + 8 * NFP;  // F', Y''
   // zero-padded rows of r''_p for the product: row (a2,a3) at rowid * RS (RS = N+1 rounded up to an
@@ -158,7 +171,7 @@ struct StageCfg {
   static constexpr int PER_E = rup(O_X + cmax(XSIZE + YSIZE, TRIPLE ? T_WSIZE : WSIZE), VEC);
   static constexpr int EB = PER_E * RB;  // element stride in bytes
   static constexpr int GB = ET * EB;     // group stride in bytes
-  static constexpr int SMEM_BYTES = G * GB + 8 * G;  // + one mbarrier per group (TMA bulk loads)
+  static constexpr int SMEM_BYTES = G * GB + 16 * G;  // + one mbarrier and one work-queue ticket per group
   static constexpr int GPW = TG < 32 ? 32 / TG : 1;  // groups per warp (sub-warp groups for small N)
   static_assert((TG % 32 == 0 || 32 % TG == 0) && T % TG == 0 && (TG <= 32 || G <= 15), "bad group shape");
 };
@@ -269,6 +282,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 #endif
 #ifndef BBW_FLUX_LATE
 #define BBW_FLUX_LATE 0  // fluxes (B1b) after C1: measured -6 % at (7,4) and -5 % at (5,3) (register spills; rejected)
+#endif
+#ifndef BBW_DYNQ
+#define BBW_DYNQ 1  // batches handed out by a global atomic ticket (tight in-flight window: neighbour traces hit L2)
 #endif
 #ifndef BBW_TMA_MIN_TG
 #define BBW_TMA_MIN_TG 32  // TMA only for whole-warp groups (sub-warp groups: cp.async; see the kernel)
@@ -1082,7 +1098,42 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
   // Sub-warp groups (TG < 32) share their warp's synchronisation, so the trip count is uniform per
   // warp: the loop runs over the batch of the warp's first group, idle groups get nE = 0.
   const int gw = grp % C::GPW;
+#if BBW_DYNQ
+  // Dynamic work queue: each warp (sub-warp groups) or group takes the next GPW batches from a global atomic
+  // ticket, so the elements in flight stay a contiguous Morton window even when SMs drift apart over the
+  // ~1700 batches per group of a 4M-element launch (a static grid-stride schedule lets the window spread,
+  // and the neighbour face traces then miss L2).  The last unit to finish resets the counters, so the next
+  // stream-ordered launch (or graph replay) starts from zero.
+  auto next_batch = [&]() -> long long {
+    if constexpr (TG <= 32) {
+      unsigned v = 0;
+      if ((tid & 31) == 0) v = atomicAdd(A.qctr, 1u);
+      return (long long)__shfl_sync(0xffffffffu, v, 0) * C::GPW;
+    } else {
+      unsigned* tslot = reinterpret_cast<unsigned*>(smem_raw + C::G * C::GB + 8 * C::G) + grp;
+      if (q == 0) *tslot = atomicAdd(A.qctr, 1u);
+      sync();
+      return (long long)*tslot;
+    }
+  };
+  // A ticket covers QCH consecutive unit-batches: 1 keeps the window tightest (best on the 4M-element config-5
+  // mesh), 2 amortises the atomic's L2 round trip on smaller meshes (api.cu picks it; drawing the next ticket at
+  // the start of a batch instead measured 2.6 % slower at (7,4)).
+  const int QCH = A.qch > 0 ? A.qch : 1;
+  long long bw = 0;
+  int qleft = 0;
+  for (;;) {
+    if (qleft == 0) {
+      bw = next_batch() * QCH;
+      qleft = QCH;
+    } else {
+      bw += C::GPW;
+    }
+    --qleft;
+    if (bw >= nbatch) break;
+#else
   for (long long bw = (long long)blockIdx.x * C::G + (grp - gw); bw < nbatch; bw += (long long)gridDim.x * C::G) {
+#endif
     const long long batch = bw + gw;
     const long long k0 = A.elem_begin + batch * ET;
     long long pt_prev = clock64();
@@ -1457,7 +1508,7 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
               const char* ya = gb + (C::Y_Y + ff * (NFP1 + 1)) * RB + u * EB;
               const R y = ld<R>(ya + o.x) + ld<R>(ya + o.y) + ld<R>(ya + o.z);
               const R F = ld<R>(gb + u * EB + (C::Y_F + ff * NFP + c) * RB);
-              st<R>(gb + u * EB + (C::X_L + ff * NP + c) * RB, fma(sc, y, R(2 * N + 3) * F));
+              st<R>(gb + u * EB + (C::X_L + ff * C::FS + c) * RB, fma(sc, y, R(2 * N + 3) * F));
             }
         }
       }
@@ -1487,6 +1538,79 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
 #define BBW_SU(u, d, k) su[u][d][k]
 #endif
       // ---- D: lift layers j = 1..N: w'_j[d] = sum_s w'_{j-1}[d + e_s]
+      if constexpr (C::ROWD) {
+        // Row ownership: lane (ff, p) owns rows p and N - p (fixed c2, contiguous in c1) of face array ff at
+        // every layer and keeps them in registers, so an output row needs only ONE other row from shared
+        // memory (row c2 + 1 of the previous layer: the d + e2 operand; d + e0 and d + e1 are its own row)
+        // instead of three operands per output.  Same arithmetic and summation order as face_sum3 (bitwise).
+        constexpr int P = (N + 2) / 2;  // lanes per face array
+        const int ff = q / P, p = q - ff * P;
+        const bool act = ff < 8;
+        const bool hasB = act && (N - p > p);
+        const int rB = N - p;
+        char* fa = gb + (C::X_L + (act ? ff : 0) * C::FS) * RB;
+        R xa[N + 2], xb[P + 1];
+        {
+          const char* pa0 = fa + (p * (2 * N + 3 - p) / 2) * RB;
+          const char* pb0 = fa + (rB * (2 * N + 3 - rB) / 2) * RB;
+          static_for<0, N + 1, 1>([&](auto cc) {
+            constexpr int c1 = decltype(cc)::value;
+            if (act && c1 <= N - p) xa[c1] = ld<R>(pa0 + c1 * RB);
+          });
+          static_for<0, P, 1>([&](auto cc) {
+            constexpr int c1 = decltype(cc)::value;
+            if (hasB && c1 <= p) xb[c1] = ld<R>(pb0 + c1 * RB);
+          });
+        }
+        static_for<1, N + 1, 1>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          constexpr int m = N - j;
+          constexpr double MU = double(-j) / double(j + 1);
+          if constexpr (j == 1) zero_region<C>(gb, q, C::Y_RPP, C::NS);  // padded r'' rows (F', Y'' are dead)
+          // slot A: row p of degree m (p <= m), length m + 1 - p; operand row p + 1 of degree m + 1
+          if (act && p <= m) {
+            const char* ps = fa + (layer_off(N, j - 1) + (p + 1) * (2 * (m + 1) + 3 - (p + 1)) / 2) * RB;
+            char* pd = fa + (layer_off(N, j) + p * (2 * m + 3 - p) / 2) * RB;
+            R nb[m + 1];
+            static_for<0, m + 1, 1>([&](auto cc) {
+              constexpr int c1 = decltype(cc)::value;
+              if (c1 <= m - p) nb[c1] = ld<R>(ps + c1 * RB);
+            });
+            static_for<0, m + 1, 1>([&](auto cc) {
+              constexpr int c1 = decltype(cc)::value;
+              if (c1 <= m - p) {
+                R v = (xa[c1] + xa[c1 + 1]) + nb[c1];
+                v *= R(MU);
+                st<R>(pd + c1 * RB, v);
+                xa[c1] = v;
+              }
+            });
+          }
+          // slot B: row N - p of degree m (needs p >= j), length p + 1 - j <= P - j; operand row N - p + 1
+          if constexpr (P - j > 0) {
+            if (hasB && p >= j) {
+              const char* ps = fa + (layer_off(N, j - 1) + (rB + 1) * (2 * (m + 1) + 3 - (rB + 1)) / 2) * RB;
+              char* pd = fa + (layer_off(N, j) + rB * (2 * m + 3 - rB) / 2) * RB;
+              R nb[P - j];
+              static_for<0, P - j, 1>([&](auto cc) {
+                constexpr int c1 = decltype(cc)::value;
+                if (c1 <= p - j) nb[c1] = ld<R>(ps + c1 * RB);
+              });
+              static_for<0, P - j, 1>([&](auto cc) {
+                constexpr int c1 = decltype(cc)::value;
+                if (c1 <= p - j) {
+                  R v = (xb[c1] + xb[c1 + 1]) + nb[c1];
+                  v *= R(MU);
+                  st<R>(pd + c1 * RB, v);
+                  xb[c1] = v;
+                }
+              });
+            }
+          }
+          sync();
+          BBW_PT(4);
+        });
+      } else
       static_for<1, N + 1, 1>([&](auto jc) {
         constexpr int j = decltype(jc)::value;
         constexpr int m = N - j;
@@ -1536,8 +1660,8 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
               R sp = R(0), sx = R(0), sy = R(0), sz = R(0);
 #pragma unroll
               for (int f = 0; f < 4; ++f) {
-                const R wp = ld<R>(eb + (C::X_L + (2 * f) * NP) * RB + lo[f]);  // lam_{a_f} already applied (D)
-                const R wu = ld<R>(eb + (C::X_L + (2 * f + 1) * NP) * RB + lo[f]);
+                const R wp = ld<R>(eb + (C::X_L + (2 * f) * C::FS) * RB + lo[f]);  // lam_{a_f} already applied (D)
+                const R wu = ld<R>(eb + (C::X_L + (2 * f + 1) * C::FS) * RB + lo[f]);
                 sp += wp;
                 sx = fma(nrm[u][3 * f], wu, sx);
                 sy = fma(nrm[u][3 * f + 1], wu, sy);
@@ -1655,6 +1779,21 @@ __global__ void __launch_bounds__(C::T, C::MINB) stage_kernel(const StageArgs<R>
     sync();
     BBW_PT(10);
   }
+#if BBW_DYNQ
+  {
+    // every unit has drawn its failing ticket before it counts itself done: the last one resets the queue
+    const bool leader = (TG <= 32) ? ((tid & 31) == 0) : (q == 0);
+    if (leader) {
+      const unsigned units = gridDim.x * (TG <= 32 ? C::T / 32 : C::G);
+      __threadfence();
+      if (atomicAdd(A.qctr + 1, 1u) == units - 1) {
+        A.qctr[0] = 0;
+        A.qctr[1] = 0;
+        __threadfence();
+      }
+    }
+  }
+#endif
 #if BBW_LSRK_TMEM
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
