@@ -488,6 +488,10 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
     const int b = atoi(e);
     if (b > 0 && b < c->ks.blocks_per_sm()) c->grid = nsm * b;
   }
+  if (const char* e = getenv("BBWADG_FORCE_BLOCKS_PER_SM")) {  // tuning: override the occupancy query (TMEM study)
+    const int b = atoi(e);
+    if (b > 0) c->grid = nsm * b;
+  }
   // NULL selects the legacy default stream (stream 0), so that work is ordered with
   // torch's default stream and every other legacy-stream user (cuBLAS convention).
   c->stream = shared_stream ? shared_stream : static_cast<cudaStream_t>(o.cuda_stream);
