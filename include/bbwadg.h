@@ -32,7 +32,17 @@
  * set_state/get_state are caller-owned, must live on the context's device,
  * use the canonical layout and the context's dtype (double for BBWADG_F64,
  * float for BBWADG_F32).  All device work is ordered on the context's stream.
- * A context is not thread-safe.
+ * A context is not thread-safe, and its kernels must not run concurrently with
+ * each other: the stage kernels take element batches from a per-context work
+ * queue counter (device memory owned by the context, reset by each launch's
+ * last CTA), so two stage launches of one context on different streams at the
+ * same time would share it.  Stream-ordered use through this API never does.
+ *
+ * Tuning environment variables (read at setup; not needed in normal use):
+ * BBWADG_BLOCKS_PER_SM=b lowers the persistent grid to b CTAs per SM;
+ * BBWADG_FORCE_BLOCKS_PER_SM=b sets it regardless of the occupancy query;
+ * BBWADG_PHASE_TIMING allocates per-phase cycle counters (timing builds);
+ * BBWADG_NO_GRAPH disables the CUDA-graph replay of bbwadg_run.
  *
  * Errors: every call returns a bbwadg_status; nothing aborts or throws across
  * the ABI.  bbwadg_error_string(ctx) (or bbwadg_last_error() when no context
