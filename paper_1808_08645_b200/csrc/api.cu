@@ -83,6 +83,7 @@ struct bbwadg_ctx_s {
   int* d_sendfaces = nullptr;
   int* d_flag = nullptr;
   unsigned int* d_qctr = nullptr;  // stage-kernel work queue: [0] next batch ticket, [1] finished units
+  int qch_elastic = 1;             // elastic kernel: unit-batches per ticket (BBWADG_ELASTIC_QCH, A/B knob)
   unsigned long long* d_ptime = nullptr;  // phase timing counters (BBW_PHASE_TIMING builds)
   // peer-read halo (halo_transport 1): owner-rank / owner-local id per ghost slot, and the peers' two
   // state buffers (same-process group members, or CUDA-IPC mappings of other processes)
@@ -174,6 +175,7 @@ bbwadg_status launch_elastic_typed(bbwadg_ctx c, int mode, const void* Qin, void
   a.s.rk_b = (R)rk_b;
   a.s.dt = (R)dt;
   a.s.mode = mode;
+  a.s.qch = c->qch_elastic;
   a.mat = static_cast<const R*>(c->d_c2);
   a.tau_s = (R)c->tau_p;  // elastic contexts: tau_p carries tau_sigma, tau_u carries tau_v (header)
   a.tau_v = (R)c->tau_u;
@@ -488,6 +490,9 @@ bbwadg_status setup_one(const GlobalMesh& g, int N, int M, const double* c2, con
     const int b = atoi(e);
     if (b > 0 && b < c->ks.blocks_per_sm()) c->grid = nsm * b;
   }
+  // elastic work-queue ticket size: 1 measured best at (7,2) (2.08 vs 2.03 / 2.00e10 for 2 / 4; (5,1), (9,2) within
+  // 0.7 %); BBWADG_ELASTIC_QCH overrides (A/B knob)
+  if (const char* e = getenv("BBWADG_ELASTIC_QCH")) c->qch_elastic = std::max(1, atoi(e));
   if (const char* e = getenv("BBWADG_FORCE_BLOCKS_PER_SM")) {  // tuning: override the occupancy query (TMEM study)
     const int b = atoi(e);
     if (b > 0) c->grid = nsm * b;

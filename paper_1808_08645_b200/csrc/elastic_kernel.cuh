@@ -109,7 +109,19 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
       return (long long)*tslot;
     }
   };
-  for (long long bw = next_batch(); bw < nelem; bw = next_batch()) {
+  // QCH unit-batches per ticket (api.cu picks it as for the acoustic kernel)
+  const int QCH = A.qch > 0 ? A.qch : 1;
+  long long bw = 0;
+  int qleft = 0;
+  for (;;) {
+    if (qleft == 0) {
+      bw = next_batch() * QCH;
+      qleft = QCH;
+    } else {
+      bw += EC::GPW;
+    }
+    --qleft;
+    if (bw >= nelem) break;
 #else
   for (long long bw = (long long)blockIdx.x * EC::G + (grp - gw); bw < nelem; bw += (long long)gridDim.x * EC::G) {
 #endif
