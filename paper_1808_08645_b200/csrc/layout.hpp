@@ -12,6 +12,10 @@
 #pragma once
 #include <stdint.h>
 
+#ifndef BBW_RED32
+#define BBW_RED32 1  // reduction table RED packed to 4 B per output (offset of b+e0 plus two 8-bit deltas)
+#endif
+
 namespace bbw {
 
 __host__ __device__ constexpr int lnp3(int n) { return n < 0 ? 0 : (n + 1) * (n + 2) * (n + 3) / 6; }

@@ -456,19 +456,31 @@ __device__ __forceinline__ void tm_load_reals(uint32_t taddr, int col0, R* x) {
 // dst[i] = sum_j src[off_j(i)] (4 terms) for the ET elements of the group.  The thread's
 // outputs i = q + TG k are fully unrolled; table loads use a clamped index so they can all be
 // issued before the shared-memory gathers (ILP), only the stores are predicated.
+#if BBW_RED32
+using red_entry = uint32_t;  // packed RED entry (layout.hpp): offset of b+e0 | delta(b+e2) << 16 | delta(b+e3) << 24
+#else
+using red_entry = ushort4;
+#endif
 template <class C, typename R, int CNT, int SRC, int DST>
-__device__ __forceinline__ void sum4_phase(char* gb, int q, const ushort4* __restrict__ tab) {
+__device__ __forceinline__ void sum4_phase(char* gb, int q, const red_entry* __restrict__ tab) {
   constexpr int K = (CNT + C::TG - 1) / C::TG;
-  ushort4 o[K];
+  red_entry o[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) o[k] = __ldg(tab + cmin(q + C::TG * k, CNT - 1));
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int i = q + C::TG * k;
+#if BBW_RED32
+    const char* p0 = gb + (o[k] & 0xFFFFu) + SRC * C::RB;
+    const char* p1 = p0 + C::RB;
+    const char* p2 = p0 + ((o[k] >> 16) & 0xFFu) * C::RB;
+    const char* p3 = p0 + (o[k] >> 24) * C::RB;
+#else
     const char* p0 = gb + o[k].x + SRC * C::RB;
     const char* p1 = gb + o[k].y + SRC * C::RB;
     const char* p2 = gb + o[k].z + SRC * C::RB;
     const char* p3 = gb + o[k].w + SRC * C::RB;
+#endif
     R v[C::ET];
 #pragma unroll
     for (int u = 0; u < C::ET; ++u)
@@ -678,7 +690,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   const uint8_t* tab = A.tab;
   const R* post = reinterpret_cast<const R*>(tab + L.s_post);
   const R* rowpost = reinterpret_cast<const R*>(tab + L.s_rowpost);
-  const ushort4* red = reinterpret_cast<const ushort4*>(tab + L.red);
+  const red_entry* red = reinterpret_cast<const red_entry*>(tab + L.red);
 
 #if BBW_PROD_V5
   // F (v5): h'_g = post_g * sum_{a+b=g} r''_a c''_b (Eq. mcoeff), output-row stationary with

@@ -255,7 +255,16 @@ HostTables build_tables(int N, int M, int RB) {
       const int* a = idx[i].a;
       int o[4] = {rank3(n, a[1], a[2], a[3]) * RB, rank3(n, a[1] + 1, a[2], a[3]) * RB,
                   rank3(n, a[1], a[2] + 1, a[3]) * RB, rank3(n, a[1], a[2], a[3] + 1) * RB};
+#if BBW_RED32
+      // packed: byte offset of b + e0 | (b + e2 - (b + e0)) << 16 | (b + e3 - (b + e0)) << 24, the deltas in reals
+      // (b + e1 is always the next real of the same row); 4 B per output instead of 8
+      const int dz = (o[2] - o[0]) / RB, dw = (o[3] - o[0]) / RB;
+      if (o[1] != o[0] + RB || dz < 0 || dz > 255 || dw < 0 || dw > 255 || o[0] > 0xFFFF)
+        throw std::runtime_error("RED32 packing out of range");
+      W.put<uint32_t>(L.red, red_off(n) + (int)i, (uint32_t)o[0] | ((uint32_t)dz << 16) | ((uint32_t)dw << 24));
+#else
       W.u16x4(L.red, red_off(n) + (int)i, o);
+#endif
     }
   }
   // UPW: degree n-1 -> n elevation with level weight 1/(a!)^2 (16-byte entries)
