@@ -686,6 +686,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
                                             long long& pt_prev, R* ob) {
   R* osc = ob;  // v4 path: output scales of J
   constexpr int N = C::N, M = C::M, NP = C::NP, NPH = C::NPH, RB = C::RB, ET = C::ET, EB = C::EB, TG = C::TG;
+  (void)NPH;
   constexpr TabLayout L = tab_layout(N, M, RB);
   const uint8_t* tab = A.tab;
   const R* post = reinterpret_cast<const R*>(tab + L.s_post);
@@ -792,6 +793,9 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         int dd = LMAX - 1 + sg;
         int fx = dd * (dd + 1) * (dd + 2) / 6 + g3v[k] * (2 * dd + 3 - g3v[k]) / 2 + g2v[k];
         int Dn = dd * (dd + 1) / 2;  // Nfp(d-1)
+        (void)DSTH;
+        (void)fx;
+        (void)Dn;
 #define BBW_HSTORE(xx, val)                                        \
   do {                                                             \
     if constexpr (C::TRIPLE) st<R>(gb + (DSTH + fx) * RB, (val));   \
