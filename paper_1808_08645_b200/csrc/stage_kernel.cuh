@@ -286,6 +286,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 #ifndef BBW_DYNQ
 #define BBW_DYNQ 1  // batches handed out by a global atomic ticket (tight in-flight window: neighbour traces hit L2)
 #endif
+#ifndef BBW_DEFER_ST
+#define BBW_DEFER_ST 1  // sparse phases: all outputs' loads before the stores (no store between loads)
+#endif
 #ifndef BBW_TMA_MIN_TG
 #define BBW_TMA_MIN_TG 32  // TMA only for whole-warp groups (sub-warp groups: cp.async; see the kernel)
 #endif
@@ -465,11 +468,13 @@ template <class C, typename R, int CNT, int SRC, int DST>
 __device__ __forceinline__ void sum4_phase(char* gb, int q, const red_entry* __restrict__ tab) {
   constexpr int K = (CNT + C::TG - 1) / C::TG;
   red_entry o[K];
+  R v[K][C::ET];
 #pragma unroll
   for (int k = 0; k < K; ++k) o[k] = __ldg(tab + cmin(q + C::TG * k, CNT - 1));
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int i = q + C::TG * k;
+    (void)i;
 #if BBW_RED32
     const char* p0 = gb + (o[k] & 0xFFFFu) + SRC * C::RB;
     const char* p1 = p0 + C::RB;
@@ -481,15 +486,28 @@ __device__ __forceinline__ void sum4_phase(char* gb, int q, const red_entry* __r
     const char* p2 = gb + o[k].z + SRC * C::RB;
     const char* p3 = gb + o[k].w + SRC * C::RB;
 #endif
-    R v[C::ET];
 #pragma unroll
     for (int u = 0; u < C::ET; ++u)
-      v[u] = (ld<R>(p0 + u * C::EB) + ld<R>(p1 + u * C::EB)) + (ld<R>(p2 + u * C::EB) + ld<R>(p3 + u * C::EB));
+      v[k][u] = (ld<R>(p0 + u * C::EB) + ld<R>(p1 + u * C::EB)) + (ld<R>(p2 + u * C::EB) + ld<R>(p3 + u * C::EB));
+#if !BBW_DEFER_ST
     if ((CNT % C::TG == 0) || i < CNT) {
 #pragma unroll
-      for (int u = 0; u < C::ET; ++u) st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v[u]);
+      for (int u = 0; u < C::ET; ++u) st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v[k][u]);
+    }
+#endif
+  }
+#if BBW_DEFER_ST
+  // stores after all loads: a store between two outputs' loads would order them (the compiler cannot prove
+  // SRC and DST disjoint), serialising one shared-memory round trip per output
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = q + C::TG * k;
+    if ((CNT % C::TG == 0) || i < CNT) {
+#pragma unroll
+      for (int u = 0; u < C::ET; ++u) st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v[k][u]);
     }
   }
+#endif
 }
 
 // dst_ff[i] = scale(i) * sum_s src_ff[off_s(i)] (3 terms) for the 8 face/flux arrays, ET elements.
@@ -518,6 +536,7 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
       const char* p0 = gb + o[k].x + SRC * C::RB;
       const char* p1 = gb + o[k].y + SRC * C::RB;
       const char* p2 = gb + o[k].z + SRC * C::RB;
+      R vv[8][C::ET];
 #pragma unroll
       for (int ff = 0; ff < 8; ++ff)
 #pragma unroll
@@ -526,8 +545,15 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
           R v = ld<R>(p0 + so) + ld<R>(p1 + so) + ld<R>(p2 + so);
           if constexpr (SCALED) v *= sc[k];
           if constexpr (SNUM != SDEN) v *= R(MU);
-          st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, v);
+          vv[ff][u] = v;
+          if constexpr (!BBW_DEFER_ST) st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, v);
         }
+      if constexpr (BBW_DEFER_ST) {  // the 8 arrays' stores after their loads (see sum4_phase)
+#pragma unroll
+        for (int ff = 0; ff < 8; ++ff)
+#pragma unroll
+          for (int u = 0; u < C::ET; ++u) st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, vv[ff][u]);
+      }
     }
   } else {
     if (q < NG * CNT) {
@@ -539,6 +565,7 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
       const char* p1 = gb + o.y + SRC * C::RB + fo;
       const char* p2 = gb + o.z + SRC * C::RB + fo;
       char* d = gb + (DST + g * GF * DSTRIDE + i) * C::RB;
+      R vv[GF][C::ET];
 #pragma unroll
       for (int ff = 0; ff < GF; ++ff)
 #pragma unroll
@@ -547,8 +574,15 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
           R v = ld<R>(p0 + so) + ld<R>(p1 + so) + ld<R>(p2 + so);
           if constexpr (SCALED) v *= sc;
           if constexpr (SNUM != SDEN) v *= R(MU);
-          st<R>(d + ff * DSTRIDE * C::RB + u * C::EB, v);
+          vv[ff][u] = v;
+          if constexpr (!BBW_DEFER_ST) st<R>(d + ff * DSTRIDE * C::RB + u * C::EB, v);
         }
+      if constexpr (BBW_DEFER_ST) {
+#pragma unroll
+        for (int ff = 0; ff < GF; ++ff)
+#pragma unroll
+          for (int u = 0; u < C::ET; ++u) st<R>(d + ff * DSTRIDE * C::RB + u * C::EB, vv[ff][u]);
+      }
     }
   }
 }
@@ -1028,6 +1062,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         o[k] = __ldg(reinterpret_cast<const ushort4*>(up + 16 * ic));
         w[k] = gn * __ldg(reinterpret_cast<const R*>(up + 16 * ic + 8));
       }
+      R v[K][ET];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int i = q + TG * k;
@@ -1035,15 +1070,24 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
         const char* p1 = gb + o[k].y + SRC * RB;
         const char* p2 = gb + o[k].z + SRC * RB;
         const char* p3 = gb + o[k].w + SRC * RB;
-        R v[ET];
 #pragma unroll
         for (int u = 0; u < ET; ++u) {
-          v[u] = (ld<R>(p0 + u * EB) + ld<R>(p1 + u * EB)) + (ld<R>(p2 + u * EB) + ld<R>(p3 + u * EB));
-          v[u] = fma(w[k], ld<R>(gb + (C::lev(n) + cmin(i, CNT - 1)) * RB + u * EB), v[u]);
+          v[k][u] = (ld<R>(p0 + u * EB) + ld<R>(p1 + u * EB)) + (ld<R>(p2 + u * EB) + ld<R>(p3 + u * EB));
+          v[k][u] = fma(w[k], ld<R>(gb + (C::lev(n) + cmin(i, CNT - 1)) * RB + u * EB), v[k][u]);
         }
-        if ((CNT % TG == 0) || i < CNT) {
+        if (!BBW_DEFER_ST && ((CNT % TG == 0) || i < CNT)) {
 #pragma unroll
-          for (int u = 0; u < ET; ++u) st<R>(gb + (DST + i) * RB + u * EB, v[u]);
+          for (int u = 0; u < ET; ++u) st<R>(gb + (DST + i) * RB + u * EB, v[k][u]);
+        }
+      }
+      if constexpr (BBW_DEFER_ST) {  // in place: lane-private u_n[i] is read above before its own store here
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int i = q + TG * k;
+          if ((CNT % TG == 0) || i < CNT) {
+#pragma unroll
+            for (int u = 0; u < ET; ++u) st<R>(gb + (DST + i) * RB + u * EB, v[k][u]);
+          }
         }
       }
     }
