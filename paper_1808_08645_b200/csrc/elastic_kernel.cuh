@@ -34,6 +34,7 @@ struct ElasticCfg {
   static constexpr int RB = AC::RB, VEC = AC::VEC, TG = AC::TG, KO = AC::KO, ET = 1;
   static constexpr int T = elastic_threads(TG);
   static constexpr int G = T / TG, GPW = TG < 32 ? 32 / TG : 1;
+  static constexpr bool DEFER = false;  // store deferral of the sparse phases: -2.2 % at (7,2) (register pressure)
   // per-element layout (reals): the acoustic block [0, AC::PER_E) (GEO at 0, c'' of the current WADG
   // application at AC::O_C, WADG work region from AC::O_X), with the elastic volume/surface arrays
   // overlaying [O_X, ...) and the three material arrays after everything
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(EC::T, EC::MINB) elastic_stage_kernel(const El
         for (int b = q; b < MP; b += TG) st<R>(gb + (AC::O_C + b) * RB, ld<R>(gb + (EC::ECM + w * MP + b) * RB));
         sync();
         R ob[KO];
-        wadg_phases<AC, R>(gb, q, A, sync, pt_prev, ob);
+        wadg_phases<AC, R, EC::DEFER>(gb, q, A, sync, pt_prev, ob);
         constexpr int RES = AC::TRIPLE ? AC::tlev(N) : wadg_result<AC>();
 #pragma unroll
         for (int kk = 0; kk < KO; ++kk) {

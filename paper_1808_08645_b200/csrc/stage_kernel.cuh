@@ -72,6 +72,9 @@ struct StageArgs {
 #ifndef BBW_T
 #define BBW_T 128
 #endif
+#ifndef BBW_DEFER_ST
+#define BBW_DEFER_ST 1  // sparse phases: all outputs' loads before the stores (no store between loads)
+#endif
 
 // default group shape per N: threads per group and elements per group-batch
 // default group shape per N (A/B-measured, scripts/ab_subwarp*.sh): sub-warp groups of TG = 4 / 4 / 8 / 16
@@ -119,6 +122,7 @@ struct StageCfg {
   // +1.9 % at (5,3); 8 CTAs spills and is slower), the fp64 choice elsewhere
   static constexpr int MINB = (sizeof(R) == 4 && N >= 5 && N <= 7) ? 6 : default_minb(N);
 #endif
+  static constexpr bool DEFER = BBW_DEFER_ST != 0;  // sparse phases store after all loads (elastic: off, measured)
   static constexpr int G = T / TG;               // groups per CTA
   static constexpr int KO = (NP + TG - 1) / TG;  // owned coefficients per thread
   // ---- per-element shared-memory layout (in reals)
@@ -285,9 +289,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 #endif
 #ifndef BBW_DYNQ
 #define BBW_DYNQ 1  // batches handed out by a global atomic ticket (tight in-flight window: neighbour traces hit L2)
-#endif
-#ifndef BBW_DEFER_ST
-#define BBW_DEFER_ST 1  // sparse phases: all outputs' loads before the stores (no store between loads)
 #endif
 #ifndef BBW_TMA_MIN_TG
 #define BBW_TMA_MIN_TG 32  // TMA only for whole-warp groups (sub-warp groups: cp.async; see the kernel)
@@ -464,7 +465,7 @@ using red_entry = uint32_t;  // packed RED entry (layout.hpp): offset of b+e0 | 
 #else
 using red_entry = ushort4;
 #endif
-template <class C, typename R, int CNT, int SRC, int DST>
+template <class C, typename R, int CNT, int SRC, int DST, bool DEFER = C::DEFER>
 __device__ __forceinline__ void sum4_phase(char* gb, int q, const red_entry* __restrict__ tab) {
   constexpr int K = (CNT + C::TG - 1) / C::TG;
   red_entry o[K];
@@ -489,25 +490,23 @@ __device__ __forceinline__ void sum4_phase(char* gb, int q, const red_entry* __r
 #pragma unroll
     for (int u = 0; u < C::ET; ++u)
       v[k][u] = (ld<R>(p0 + u * C::EB) + ld<R>(p1 + u * C::EB)) + (ld<R>(p2 + u * C::EB) + ld<R>(p3 + u * C::EB));
-#if !BBW_DEFER_ST
-    if ((CNT % C::TG == 0) || i < CNT) {
-#pragma unroll
-      for (int u = 0; u < C::ET; ++u) st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v[k][u]);
-    }
-#endif
-  }
-#if BBW_DEFER_ST
-  // stores after all loads: a store between two outputs' loads would order them (the compiler cannot prove
-  // SRC and DST disjoint), serialising one shared-memory round trip per output
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int i = q + C::TG * k;
-    if ((CNT % C::TG == 0) || i < CNT) {
+    if (!DEFER && ((CNT % C::TG == 0) || i < CNT)) {
 #pragma unroll
       for (int u = 0; u < C::ET; ++u) st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v[k][u]);
     }
   }
-#endif
+  if constexpr (DEFER) {
+    // stores after all loads: a store between two outputs' loads would order them (the compiler cannot prove
+    // SRC and DST disjoint), serialising one shared-memory round trip per output
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int i = q + C::TG * k;
+      if ((CNT % C::TG == 0) || i < CNT) {
+#pragma unroll
+        for (int u = 0; u < C::ET; ++u) st<R>(gb + DST * C::RB + u * C::EB + i * C::RB, v[k][u]);
+      }
+    }
+  }
 }
 
 // dst_ff[i] = scale(i) * sum_s src_ff[off_s(i)] (3 terms) for the 8 face/flux arrays, ET elements.
@@ -546,9 +545,9 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
           if constexpr (SCALED) v *= sc[k];
           if constexpr (SNUM != SDEN) v *= R(MU);
           vv[ff][u] = v;
-          if constexpr (!BBW_DEFER_ST) st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, v);
+          if constexpr (!C::DEFER) st<R>(gb + (DST + ff * DSTRIDE + i) * C::RB + u * C::EB, v);
         }
-      if constexpr (BBW_DEFER_ST) {  // the 8 arrays' stores after their loads (see sum4_phase)
+      if constexpr (C::DEFER) {  // the 8 arrays' stores after their loads (see sum4_phase)
 #pragma unroll
         for (int ff = 0; ff < 8; ++ff)
 #pragma unroll
@@ -575,9 +574,9 @@ __device__ __forceinline__ void face_sum3(char* gb, int q, const ushort4* __rest
           if constexpr (SCALED) v *= sc;
           if constexpr (SNUM != SDEN) v *= R(MU);
           vv[ff][u] = v;
-          if constexpr (!BBW_DEFER_ST) st<R>(d + ff * DSTRIDE * C::RB + u * C::EB, v);
+          if constexpr (!C::DEFER) st<R>(d + ff * DSTRIDE * C::RB + u * C::EB, v);
         }
-      if constexpr (BBW_DEFER_ST) {
+      if constexpr (C::DEFER) {
 #pragma unroll
         for (int ff = 0; ff < GF; ++ff)
 #pragma unroll
@@ -715,7 +714,7 @@ __device__ __forceinline__ void tri_projection(char* gb, int q, const StageArgs<
   });
 }
 
-template <class C, typename R>
+template <class C, typename R, bool DEFER = C::DEFER>
 __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>& A, const GroupSync<C>& sync,
                                             long long& pt_prev, R* ob) {
   R* osc = ob;  // v4 path: output scales of J
@@ -1009,7 +1008,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
     constexpr int k = N + M - n;
     constexpr int SRC = (k % 2 == 0) ? C::W_H : C::W_P;
     constexpr int DST = (n - 1 == N) ? C::lev(N) : ((k % 2 == 0) ? C::W_P : C::W_H);
-    sum4_phase<C, R, cnp3(n - 1), SRC, DST>(gb, q, red + red_off(n));
+    sum4_phase<C, R, cnp3(n - 1), SRC, DST, DEFER>(gb, q, red + red_off(n));
     sync();
     BBW_PT(7);
   });
@@ -1031,7 +1030,7 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
   // H: downward reductions level n -> n-1
   static_for<N, 0, -1>([&](auto nc) {
     constexpr int n = decltype(nc)::value;
-    sum4_phase<C, R, cnp3(n - 1), C::lev(n), C::lev(n - 1)>(gb, q, red + red_off(n));
+    sum4_phase<C, R, cnp3(n - 1), C::lev(n), C::lev(n - 1), DEFER>(gb, q, red + red_off(n));
     sync();
     BBW_PT(8);
   });
@@ -1075,12 +1074,12 @@ __device__ __forceinline__ void wadg_phases(char* gb, int q, const StageArgs<R>&
           v[k][u] = (ld<R>(p0 + u * EB) + ld<R>(p1 + u * EB)) + (ld<R>(p2 + u * EB) + ld<R>(p3 + u * EB));
           v[k][u] = fma(w[k], ld<R>(gb + (C::lev(n) + cmin(i, CNT - 1)) * RB + u * EB), v[k][u]);
         }
-        if (!BBW_DEFER_ST && ((CNT % TG == 0) || i < CNT)) {
+        if (!DEFER && ((CNT % TG == 0) || i < CNT)) {
 #pragma unroll
           for (int u = 0; u < ET; ++u) st<R>(gb + (DST + i) * RB + u * EB, v[k][u]);
         }
       }
-      if constexpr (BBW_DEFER_ST) {  // in place: lane-private u_n[i] is read above before its own store here
+      if constexpr (DEFER) {  // in place: lane-private u_n[i] is read above before its own store here
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const int i = q + TG * k;
